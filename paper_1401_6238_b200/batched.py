@@ -1,0 +1,159 @@
+"""Batched device API over torch CUDA tensors (the engine under the drop-in).
+
+Every function here launches the sm_100a kernels of ``libhankelfft_b200.so``
+asynchronously on the current torch CUDA stream and returns device tensors;
+nothing synchronises.  Inputs are complex128 (or float64, promoted on the fly
+like the reference's ``core.as_complex``, core.py:21-22).
+
+Shapes (B = batch of independent tensors):
+  h     : (B, d_H) generating vectors, or (B, L) spectra from ``hankel_spectrum``
+  xs[p] : (B, n_{p+2}) for partial products, (B, n_{p+1}) for full products;
+          passing the SAME tensor object twice means "same vector" (one FFT).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native as N
+
+
+def _require_cuda(t: torch.Tensor, name: str) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU path exists)")
+
+
+def _operand(t: torch.Tensor, name: str, spectrum: bool = False) -> N.Operand:
+    _require_cuda(t, name)
+    if t.dim() != 2:
+        raise ValueError(f"{name} must be 2-D (batch, length)")
+    if t.stride(1) != 1:
+        raise ValueError(f"{name} must be contiguous along its last dimension")
+    if t.dtype == torch.complex128:
+        dt = N.HK_SPEC if spectrum else N.HK_C128
+    elif t.dtype == torch.float64 and not spectrum:
+        dt = N.HK_F64
+    else:
+        raise ValueError(f"{name} must be complex128{'' if spectrum else ' or float64'}")
+    return N.Operand(t.data_ptr(), t.stride(0), dt, 0)
+
+
+def _stream(device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _dev_index(t: torch.Tensor) -> int:
+    return t.device.index if t.device.index is not None else torch.cuda.current_device()
+
+
+def hankel_plan(shape, device: int, fft_len: int = 0) -> N.Plan:
+    return N.hankel_plan(shape, device, fft_len)
+
+
+def hankel_spectrum(h: torch.Tensor, shape, fft_len: int = 0) -> torch.Tensor:
+    """Batched cached spectrum S = ifft(h~) (reference hankel.py:37-40, 126-128).
+
+    Returns (B, L) complex128 in the library's internal layout (opaque: only
+    meaningful as the ``h`` argument of the product functions).
+    """
+    dev = _dev_index(h)
+    with torch.cuda.device(dev):
+        plan = hankel_plan(shape, dev, fft_len)
+        B = h.shape[0]
+        spec = torch.empty((B, plan.spectrum_len), dtype=torch.complex128, device=h.device)
+        N.check(N.load_library().hk_spectrum(plan.handle, _operand(h, "h"), B, spec.data_ptr(),
+                                             None, _stream(dev)), "hk_spectrum")
+    return spec
+
+
+def _vector_operands(xs, names):
+    ops = (N.Operand * len(xs))()
+    for i, x in enumerate(xs):
+        ops[i] = _operand(x, names[i])
+    return ops
+
+
+def hankel_tvp_partial(h: torch.Tensor, xs, shape, *, spectrum: bool = False,
+                       out: torch.Tensor | None = None, fft_len: int = 0) -> torch.Tensor:
+    """y_b = H_b x_{b,2} ... x_{b,m} (reference hankel.py:140-147), batched.
+
+    Returns (B, n_1) complex128.  ``spectrum=True`` means ``h`` holds cached
+    spectra from :func:`hankel_spectrum` with the same shape/fft_len.
+    """
+    shape = tuple(int(n) for n in shape)
+    m = len(shape)
+    xs = list(xs)
+    if len(xs) != m - 1:
+        raise ValueError(f"expected {m - 1} vectors, got {len(xs)}")
+    dev = _dev_index(h)
+    B = h.shape[0]
+    with torch.cuda.device(dev):
+        plan = hankel_plan(shape, dev, fft_len)
+        if out is None:
+            out = torch.empty((B, shape[0]), dtype=torch.complex128, device=h.device)
+        _require_cuda(out, "out")
+        ops = _vector_operands(xs, [f"xs[{i}]" for i in range(len(xs))])
+        N.check(N.load_library().hk_tvp_partial(
+            plan.handle, _operand(h, "h", spectrum), ops, len(xs), B, out.data_ptr(),
+            out.stride(0), None, _stream(dev)), "hk_tvp_partial")
+    return out
+
+
+def hankel_tvp_full(h: torch.Tensor, xs, shape, *, spectrum: bool = False,
+                    fft_len: int = 0) -> torch.Tensor:
+    """alpha_b = H_b x_1 ... x_m, unconjugated (reference hankel.py:149-154). (B,) complex128."""
+    shape = tuple(int(n) for n in shape)
+    m = len(shape)
+    xs = list(xs)
+    if len(xs) != m:
+        raise ValueError(f"expected {m} vectors, got {len(xs)}")
+    dev = _dev_index(h)
+    B = h.shape[0]
+    with torch.cuda.device(dev):
+        plan = hankel_plan(shape, dev, fft_len)
+        alpha = torch.empty((B,), dtype=torch.complex128, device=h.device)
+        ops = _vector_operands(xs, [f"xs[{i}]" for i in range(len(xs))])
+        N.check(N.load_library().hk_tvp_full(
+            plan.handle, _operand(h, "h", spectrum), ops, len(xs), B, alpha.data_ptr(), None,
+            _stream(dev)), "hk_tvp_full")
+    return alpha
+
+
+def times_matrices(h: torch.Tensor, shape, mats, *, spectrum: bool = False,
+                   fft_len: int = 0) -> torch.Tensor:
+    """T_b[:, j_2..j_m] = H_b x_2 M_2[:, j_2] ... (reference hankel.py:174-194).
+
+    mats[p]: (B, n_{p+2}, R_p) complex128 (row-major per item).  Passing the
+    same tensor object for several modes shares its column spectra.
+    Returns (B, n_1, R_2, ..., R_m) complex128.
+    """
+    shape = tuple(int(n) for n in shape)
+    m = len(shape)
+    mats = list(mats)
+    if len(mats) != m - 1:
+        raise ValueError(f"expected {m - 1} matrices, got {len(mats)}")
+    dev = _dev_index(h)
+    B = h.shape[0]
+    for p, M in enumerate(mats):
+        _require_cuda(M, f"mats[{p}]")
+        if M.dim() != 3 or M.shape[1] != shape[p + 1] or M.dtype != torch.complex128:
+            raise ValueError(f"matrix {p} must be (B, {shape[p + 1]}, R) complex128")
+        if M.stride(2) != 1 or M.stride(1) != M.shape[2]:
+            raise ValueError(f"matrix {p} must be row-major contiguous per item")
+    ranks = [int(M.shape[2]) for M in mats]
+    with torch.cuda.device(dev):
+        plan = hankel_plan(shape, dev, fft_len)
+        lib = N.load_library()
+        r_arr = N.i64_array(ranks)
+        ws_bytes = lib.hk_times_matrices_workspace_bytes(plan.handle, r_arr, len(mats), B)
+        ws = torch.empty((max(int(ws_bytes), 16),), dtype=torch.uint8, device=h.device)
+        T = torch.empty((B, shape[0], *ranks), dtype=torch.complex128, device=h.device)
+        ptrs = (ctypes.c_void_p * len(mats))(*[M.data_ptr() for M in mats])
+        strides = N.i64_array([M.stride(0) for M in mats])
+        N.check(lib.hk_times_matrices(plan.handle, _operand(h, "h", spectrum), ptrs, strides,
+                                      r_arr, len(mats), B, T.data_ptr(),
+                                      T[0].numel() if B else 0, ws.data_ptr(), _stream(dev)),
+                "hk_times_matrices")
+    return T

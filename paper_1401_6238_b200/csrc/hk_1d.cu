@@ -1,0 +1,199 @@
+// K1 / K2: fused batched 1D Hankel tensor products, one FFT length per
+// template instance, a group of T threads per product (G products per CTA).
+//
+// Per product b (reference hankel.py:140-154 via the anti-circulant
+// embedding, hankel.py:42-71):
+//   acc = ifft(h~)                       -- or the cached spectrum
+//   acc *= fft(x~_f)^{power_f}           -- one transform per DISTINCT vector
+//   partial: y = fft(acc)[:n_1]          -- transposed network, natural order out
+//   full:    alpha = sum(acc)            -- fixed-order deterministic reduction
+// The zero padding to L and the truncation to n_1 never touch memory: loads
+// beyond len return 0, stores beyond out_len are skipped.
+#include <atomic>
+
+#include "hk_fft1d.cuh"
+#include "hk_internal.h"
+
+namespace hk {
+
+__device__ __forceinline__ long long item_off(long long bstride, long long sstride, long long ob,
+                                              long long os) {
+  return ob * bstride + os * sstride;
+}
+
+__device__ __forceinline__ cplx load_factor(const Factor &f, long long off, int pos,
+                                            double scale) {
+  if (pos >= f.len) return make_double2(0.0, 0.0);
+  const long long k = (long long)pos * f.estride;
+  if (f.kind == FK_F64) {
+    const double *p = static_cast<const double *>(f.ptr) + off;
+    return make_double2(__ldg(p + k) * scale, 0.0);
+  }
+  const cplx *p = static_cast<const cplx *>(f.ptr) + off;
+  cplx v = __ldg(p + k);
+  return make_double2(v.x * scale, v.y * scale);
+}
+
+template <class PL>
+__global__ void __launch_bounds__(PL::CTA, 1) k_hankel_1d(const __grid_constant__ Args1D a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx *smem = reinterpret_cast<cplx *>(smem_raw);
+  constexpr int T = PL::T;
+  constexpr int V = PL::V;
+  const int g = threadIdx.x / T;
+  const int t = threadIdx.x - g * T;
+  long long b = (long long)blockIdx.x * PL::G + g;
+  const bool active = b < a.batch;
+  if (!active) b = a.batch - 1;  // idle groups shadow a valid item; their stores are masked
+  const long long ob = b / a.nsub, os = b - (b / a.nsub) * a.nsub;
+  cplx *sbuf = smem + (PL::P > 1 ? g * PL::L : 0);
+  const cplx *__restrict__ tw = a.tw;
+
+  cplx acc[V];
+  if (a.mode != M_SPEC_F) {
+    if (a.h.kind == FK_SPEC) {
+      const cplx *sp = static_cast<const cplx *>(a.h.ptr) + item_off(a.h.bstride, a.h.sstride, ob, os);
+#pragma unroll
+      for (int r = 0; r < V; ++r) acc[r] = __ldg(sp + r * T + t);
+    } else {
+      const Factor &hf = a.h;
+      const double sc = a.scale;
+      const long long off = item_off(hf.bstride, hf.sstride, ob, os);
+      fft_dif<PL, true>(sbuf, t, tw, [&](int pos) { return load_factor(hf, off, pos, sc); }, acc);
+    }
+  }
+
+  for (int f = 0; f < a.nfac; ++f) {
+    const Factor &fa = a.fac[f];
+    cplx w[V];
+    const long long off = item_off(fa.bstride, fa.sstride, ob, os);
+    if (fa.kind == FK_SPEC) {
+      const cplx *sp = static_cast<const cplx *>(fa.ptr) + off;
+#pragma unroll
+      for (int r = 0; r < V; ++r) w[r] = __ldg(sp + r * T + t);
+    } else {
+      fft_dif<PL, false>(sbuf, t, tw, [&](int pos) { return load_factor(fa, off, pos, 1.0); }, w);
+    }
+    if (a.mode == M_SPEC_F) {
+#pragma unroll
+      for (int r = 0; r < V; ++r) acc[r] = w[r];
+    } else {
+      for (int k = 0; k < fa.power; ++k) {
+#pragma unroll
+        for (int r = 0; r < V; ++r) acc[r] = cmul(acc[r], w[r]);
+      }
+    }
+  }
+
+  cplx *out = static_cast<cplx *>(a.out) + item_off(a.out_bstride, a.out_sstride, ob, os);
+  if (a.mode == M_PARTIAL) {
+    const int n1 = a.out_len;
+    const long long es = a.out_estride;
+    fft_dit_final<PL>(sbuf, t, tw, acc, [&](int pos, cplx v) {
+      if (active && pos < n1) out[pos * es] = v;
+    });
+  } else if (a.mode == M_FULL) {
+    cplx s = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < V; ++r) s = cadd(s, acc[r]);
+    // deterministic: per-thread partials in smem, summed in thread order
+    __syncthreads();
+    cplx *red = smem + g * T;  // G*T <= G*L slots
+    red[t] = s;
+    __syncthreads();
+    if (t == 0 && active) {
+      cplx tot = make_double2(0.0, 0.0);
+      for (int k = 0; k < T; ++k) tot = cadd(tot, red[k]);
+      out[0] = tot;
+    }
+  } else {
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < V; ++r) out[r * T + t] = acc[r];
+    }
+  }
+}
+
+template <class PL>
+static cudaError_t launch_plan(const Args1D &a, cudaStream_t stream) {
+  // M_FULL reuses smem for T partial sums; make sure it exists when P == 1.
+  int smem = PL::SMEM_BYTES;
+  const int red_bytes = PL::G * PL::T * (int)sizeof(cplx);
+  if (smem < red_bytes) smem = red_bytes;
+  static std::atomic<unsigned long long> configured{0};  // one bit per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(configured.load() & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(k_hankel_1d<PL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured.fetch_or(bit);
+  }
+  const long long grid = (a.batch + PL::G - 1) / PL::G;
+  if (grid <= 0) return cudaSuccess;
+  k_hankel_1d<PL><<<(unsigned)grid, PL::CTA, smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+// Supported on-chip lengths.  Power-of-two lengths use radix-16 passes with one
+// small leading radix; 3*2^k lengths put a radix-12/24/3/6 pass first.
+#define HK_PLAN_LIST(X)                     \
+  X(2, Plan1D<2, 1, 2>)                     \
+  X(4, Plan1D<4, 1, 4>)                     \
+  X(8, Plan1D<8, 1, 8>)                     \
+  X(16, Plan1D<16, 1, 16>)                  \
+  X(32, Plan1D<32, 2, 2, 16>)               \
+  X(64, Plan1D<64, 4, 4, 16>)               \
+  X(128, Plan1D<128, 8, 8, 16>)             \
+  X(256, Plan1D<256, 16, 16, 16>)           \
+  X(512, Plan1D<512, 32, 2, 16, 16>)        \
+  X(1024, Plan1D<1024, 64, 4, 16, 16>)      \
+  X(2048, Plan1D<2048, 128, 8, 16, 16>)     \
+  X(4096, Plan1D<4096, 256, 16, 16, 16>)    \
+  X(8192, Plan1D<8192, 512, 2, 16, 16, 16>) \
+  X(12, Plan1D<12, 1, 12>)                  \
+  X(24, Plan1D<24, 1, 24>)                  \
+  X(48, Plan1D<48, 3, 3, 16>)               \
+  X(96, Plan1D<96, 6, 6, 16>)               \
+  X(192, Plan1D<192, 12, 12, 16>)           \
+  X(384, Plan1D<384, 24, 24, 16>)           \
+  X(768, Plan1D<768, 48, 3, 16, 16>)        \
+  X(1536, Plan1D<1536, 96, 6, 16, 16>)      \
+  X(3072, Plan1D<3072, 192, 12, 16, 16>)    \
+  X(6144, Plan1D<6144, 384, 24, 16, 16>)
+
+cudaError_t launch_1d(int L, const Args1D &a, cudaStream_t stream) {
+  switch (L) {
+#define HK_CASE(len, ...) \
+  case len:              \
+    return launch_plan<__VA_ARGS__>(a, stream);
+    HK_PLAN_LIST(HK_CASE)
+#undef HK_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+bool supported_1d(long long L) {
+  switch (L) {
+#define HK_CASE(len, ...) \
+  case len:              \
+    return true;
+    HK_PLAN_LIST(HK_CASE)
+#undef HK_CASE
+    default:
+      return false;
+  }
+}
+
+long long choose_len_1d(long long d) {
+  long long best = -1;
+#define HK_CASE(len, ...) \
+  if (len >= d && (best < 0 || len < best)) best = len;
+  HK_PLAN_LIST(HK_CASE)
+#undef HK_CASE
+  return best;
+}
+
+}  // namespace hk

@@ -1,0 +1,228 @@
+// Register-resident DFT codelets for the fused Hankel product kernels.
+//
+// All radices are compile-time: loops are expanded with `sfor<N>` so every
+// array index and every twiddle constant is a constant expression, which keeps
+// the butterflies entirely in registers and turns twiddles into immediates.
+//
+// Sign convention (numpy / reference fourier.py:1-7): forward uses
+// exp(-2*pi*i*j*k/n), inverse the conjugate kernel (the 1/n factor is applied
+// by the caller).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <type_traits>
+
+namespace hk {
+
+using cplx = double2;
+
+// ---------------------------------------------------------------- compile-time loop
+template <int I, int N, class F>
+__device__ __forceinline__ void sfor_impl(F &&f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    sfor_impl<I + 1, N>(f);
+  }
+}
+template <int N, class F>
+__device__ __forceinline__ void sfor(F &&f) { sfor_impl<0, N>(f); }
+
+// ---------------------------------------------------------------- complex helpers
+__device__ __forceinline__ cplx cadd(cplx a, cplx b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ cplx csub(cplx a, cplx b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ cplx cmulc(cplx a, cplx b) {
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ cplx cscale(cplx a, double s) { return make_double2(a.x * s, a.y * s); }
+// a * (-i) and a * (+i)
+__device__ __forceinline__ cplx mul_mi(cplx a) { return make_double2(a.y, -a.x); }
+__device__ __forceinline__ cplx mul_pi(cplx a) { return make_double2(-a.y, a.x); }
+template <bool INV>
+__device__ __forceinline__ cplx cmul_dir(cplx a, cplx w) { return INV ? cmulc(a, w) : cmul(a, w); }
+
+// ---------------------------------------------------------------- constexpr twiddles
+// cos / sin of 2*pi*e/R computed at compile time: exact integer reduction to a
+// quadrant, Taylor series on |phi| <= pi/4 (error ~1 ulp).
+constexpr double kHalfPi = 1.57079632679489661923132169163975144;
+
+constexpr double taylor_sin(double x) {
+  double term = x, sum = x;
+  for (int k = 1; k < 14; ++k) {
+    term *= -x * x / ((2.0 * k) * (2.0 * k + 1.0));
+    sum += term;
+  }
+  return sum;
+}
+constexpr double taylor_cos(double x) {
+  double term = 1.0, sum = 1.0;
+  for (int k = 1; k < 14; ++k) {
+    term *= -x * x / ((2.0 * k - 1.0) * (2.0 * k));
+    sum += term;
+  }
+  return sum;
+}
+// angle 2*pi*e/R = (quarter turns) 4e/R; q = nearest integer, phi = (4e - qR)/R * pi/2
+constexpr double tw_cos(long long e, long long R) {
+  e %= R;
+  if (e < 0) e += R;
+  long long num = 4 * e;
+  long long q = (2 * num + R) / (2 * R);
+  double phi = (double)(num - q * R) / (double)R * kHalfPi;
+  double c = taylor_cos(phi), s = taylor_sin(phi);
+  switch (q & 3) {
+    case 0: return c;
+    case 1: return -s;
+    case 2: return -c;
+    default: return s;
+  }
+}
+constexpr double tw_sin(long long e, long long R) {
+  e %= R;
+  if (e < 0) e += R;
+  long long num = 4 * e;
+  long long q = (2 * num + R) / (2 * R);
+  double phi = (double)(num - q * R) / (double)R * kHalfPi;
+  double c = taylor_cos(phi), s = taylor_sin(phi);
+  switch (q & 3) {
+    case 0: return s;
+    case 1: return c;
+    case 2: return -s;
+    default: return -c;
+  }
+}
+
+// a * exp(sign * 2*pi*i*E/R), sign = -1 forward, +1 inverse; E, R compile time.
+template <int E, int R, bool INV>
+__device__ __forceinline__ cplx twc(cplx a) {
+  constexpr int e = ((E % R) + R) % R;
+  if constexpr (e == 0) {
+    return a;
+  } else if constexpr (4 * e == 2 * R) {
+    return make_double2(-a.x, -a.y);
+  } else if constexpr (4 * e == R) {
+    return INV ? mul_pi(a) : mul_mi(a);
+  } else if constexpr (4 * e == 3 * R) {
+    return INV ? mul_mi(a) : mul_pi(a);
+  } else {
+    constexpr double c = tw_cos(e, R);
+    constexpr double s = INV ? tw_sin(e, R) : -tw_sin(e, R);
+    return make_double2(fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c));
+  }
+}
+
+// ---------------------------------------------------------------- codelets
+template <int R, bool INV>
+struct Dft;
+
+template <bool INV>
+struct Dft<1, INV> {
+  __device__ __forceinline__ static void run(cplx *) {}
+};
+
+template <bool INV>
+struct Dft<2, INV> {
+  __device__ __forceinline__ static void run(cplx *v) {
+    cplx a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  }
+};
+
+template <bool INV>
+struct Dft<3, INV> {
+  __device__ __forceinline__ static void run(cplx *v) {
+    constexpr double s3 = 0.866025403784438646763723170752936183;  // sin(2pi/3)
+    cplx a = v[0], s = cadd(v[1], v[2]), d = csub(v[1], v[2]);
+    cplx m = make_double2(fma(-0.5, s.x, a.x), fma(-0.5, s.y, a.y));
+    // forward: X1 = m - i*s3*d, X2 = m + i*s3*d
+    cplx r = make_double2(-s3 * d.y, s3 * d.x);  // i*s3*d
+    v[0] = cadd(a, s);
+    if (INV) {
+      v[1] = cadd(m, r);
+      v[2] = csub(m, r);
+    } else {
+      v[1] = csub(m, r);
+      v[2] = cadd(m, r);
+    }
+  }
+};
+
+template <bool INV>
+struct Dft<4, INV> {
+  __device__ __forceinline__ static void run(cplx *v) {
+    cplx t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+    cplx t2 = cadd(v[1], v[3]), t3 = csub(v[1], v[3]);
+    t3 = INV ? mul_pi(t3) : mul_mi(t3);
+    v[0] = cadd(t0, t2);
+    v[2] = csub(t0, t2);
+    v[1] = cadd(t1, t3);
+    v[3] = csub(t1, t3);
+  }
+};
+
+constexpr int first_factor(int R) { return (R % 4 == 0 && R != 8) ? 4 : (R % 2 == 0 ? 2 : 3); }
+
+// Composite R = R1 * R2 (natural-order in and out):
+//   X[k1 + R1 k2] = sum_{n2} W_R2^{n2 k2} W_R^{n2 k1} sum_{n1} v[n1 R2 + n2] W_R1^{n1 k1}
+template <int R, bool INV>
+struct Dft {
+  static_assert(R > 4, "composite codelet");
+  static constexpr int R1 = first_factor(R);
+  static constexpr int R2 = R / R1;
+  static_assert(R1 * R2 == R, "radix must factor into 2,3,4");
+  __device__ __forceinline__ static void run(cplx *v) {
+    cplx t[R];
+    sfor<R2>([&](auto n2c) {
+      constexpr int n2 = decltype(n2c)::value;
+      cplx a[R1];
+      sfor<R1>([&](auto n1c) {
+        constexpr int n1 = decltype(n1c)::value;
+        a[n1] = v[n1 * R2 + n2];
+      });
+      Dft<R1, INV>::run(a);
+      sfor<R1>([&](auto k1c) {
+        constexpr int k1 = decltype(k1c)::value;
+        t[k1 * R2 + n2] = twc<n2 * k1, R, INV>(a[k1]);
+      });
+    });
+    sfor<R1>([&](auto k1c) {
+      constexpr int k1 = decltype(k1c)::value;
+      cplx b[R2];
+      sfor<R2>([&](auto n2c) {
+        constexpr int n2 = decltype(n2c)::value;
+        b[n2] = t[k1 * R2 + n2];
+      });
+      Dft<R2, INV>::run(b);
+      sfor<R2>([&](auto k2c) {
+        constexpr int k2 = decltype(k2c)::value;
+        v[k1 + R1 * k2] = b[k2];
+      });
+    });
+  }
+};
+
+// radix-8 as 2 x 4 keeps the W8 twiddles to the two odd slots
+template <bool INV>
+struct Dft<8, INV> {
+  __device__ __forceinline__ static void run(cplx *v) {
+    cplx e[4] = {v[0], v[2], v[4], v[6]};
+    cplx o[4] = {v[1], v[3], v[5], v[7]};
+    Dft<4, INV>::run(e);
+    Dft<4, INV>::run(o);
+    o[1] = twc<1, 8, INV>(o[1]);
+    o[2] = twc<2, 8, INV>(o[2]);
+    o[3] = twc<3, 8, INV>(o[3]);
+    sfor<4>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      v[k] = cadd(e[k], o[k]);
+      v[k + 4] = csub(e[k], o[k]);
+    });
+  }
+};
+
+}  // namespace hk

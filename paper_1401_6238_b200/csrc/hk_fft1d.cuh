@@ -1,0 +1,176 @@
+// CTA-level mixed-radix FFT engine used by the fused Hankel product kernels.
+//
+// Length L = R_0 * R_1 * ... * R_{P-1}.  Positions use the in-place
+// decimation-in-frequency layout: pass p combines the elements
+// base + j * s_p (j < R_p, s_p = L / (R_0...R_p)) and multiplies output j by
+// W_L^{j * lo * L / (s_p R_p)} with lo = base mod s_p.  After the last pass a
+// thread owns V = L / T frequency samples in digit-reversed order, in
+// registers.
+//
+// The product kernels exploit two facts:
+//  * every spectrum in a product (ifft(h), fft(x_p)) is produced with the same
+//    decomposition and thread mapping, so the pointwise product
+//    ifft(h) .* prod fft(x_p) (reference hankel.py:61-71) is a register-only
+//    operation on matching positions;
+//  * the final forward FFT (hankel.py:45) is the transpose of the DIF network
+//    (the DFT matrix is symmetric), so it consumes the digit-reversed
+//    registers directly by running the passes in reverse order with the
+//    twiddle applied before each butterfly, and emits natural-order output --
+//    no reordering step at all.
+// Passes exchange through shared memory with an XOR swizzle on 16-byte
+// elements (bits 0-2 ^= bits 4-6) that keeps every 8-lane phase of a 128-bit
+// access on distinct bank groups for the strides used here.
+#pragma once
+
+#include "hk_dft.cuh"
+
+namespace hk {
+
+template <int L_, int T_, int... Rs>
+struct Plan1D {
+  static constexpr int L = L_;
+  static constexpr int T = T_;
+  static constexpr int P = sizeof...(Rs);
+  static constexpr int radix[P] = {Rs...};
+  static constexpr int Rlast = radix[P - 1];
+  static_assert((L / Rlast) % T == 0, "last pass must split evenly over the threads");
+  static constexpr int V = L / T;  // values per thread after the last pass
+  static constexpr int prod() {
+    int r = 1;
+    for (int q = 0; q < P; ++q) r *= radix[q];
+    return r;
+  }
+  static_assert(prod() == L, "radices must multiply to L");
+  static constexpr int stride(int p) {
+    int s = L;
+    for (int q = 0; q <= p; ++q) s /= radix[q];
+    return s;
+  }
+  static constexpr int G = (T >= 256) ? 1 : 256 / T;  // independent products per CTA
+  static constexpr int CTA = G * T;
+  static constexpr int SMEM_BYTES = (P > 1) ? G * L * (int)sizeof(cplx) : 16;
+};
+
+__device__ __forceinline__ int swz(int pos) { return pos ^ ((pos >> 4) & 7); }
+
+// One DIF pass.  load(pos) -> cplx ; store(i, j, pos, value).
+template <class PL, int p, bool INV, class Load, class Store>
+__device__ __forceinline__ void dif_pass(int t, const cplx *__restrict__ tw, Load &&load,
+                                         Store &&store) {
+  constexpr int R = PL::radix[p];
+  constexpr int s = PL::stride(p);
+  constexpr int Lp = s * R;
+  constexpr int NBUT = PL::L / R;
+  constexpr int NB = (NBUT + PL::T - 1) / PL::T;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    const int beta = t + i * PL::T;
+    if (NBUT % PL::T == 0 || beta < NBUT) {
+      const int lo = beta % s;
+      const int base = (beta / s) * Lp + lo;
+      cplx a[R];
+      sfor<R>([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
+        a[j] = load(base + j * s);
+      });
+      Dft<R, INV>::run(a);
+      if constexpr (p < PL::P - 1) {
+        const int e1 = lo * (PL::L / Lp);
+        sfor<R>([&](auto jc) {
+          constexpr int j = decltype(jc)::value;
+          if constexpr (j > 0) a[j] = cmul_dir<INV>(a[j], __ldg(&tw[j * e1]));
+        });
+      }
+      sfor<R>([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
+        store(i, j, base + j * s, a[j]);
+      });
+    }
+  }
+}
+
+// One transposed (DIT) pass of the forward transform: twiddle, then butterfly.
+// load(i, j, pos) -> cplx ; store(i, j, pos, value).
+template <class PL, int p, class Load, class Store>
+__device__ __forceinline__ void dit_pass(int t, const cplx *__restrict__ tw, Load &&load,
+                                         Store &&store) {
+  constexpr int R = PL::radix[p];
+  constexpr int s = PL::stride(p);
+  constexpr int Lp = s * R;
+  constexpr int NBUT = PL::L / R;
+  constexpr int NB = (NBUT + PL::T - 1) / PL::T;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    const int beta = t + i * PL::T;
+    if (NBUT % PL::T == 0 || beta < NBUT) {
+      const int lo = beta % s;
+      const int base = (beta / s) * Lp + lo;
+      cplx a[R];
+      sfor<R>([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
+        a[j] = load(i, j, base + j * s);
+      });
+      if constexpr (p < PL::P - 1) {
+        const int e1 = lo * (PL::L / Lp);
+        sfor<R>([&](auto jc) {
+          constexpr int j = decltype(jc)::value;
+          if constexpr (j > 0) a[j] = cmul(a[j], __ldg(&tw[j * e1]));
+        });
+      }
+      Dft<R, false>::run(a);
+      sfor<R>([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
+        store(i, j, base + j * s, a[j]);
+      });
+    }
+  }
+}
+
+// Full DIF transform: global loader -> registers (digit-reversed).
+template <class PL, bool INV, class GLoad>
+__device__ __forceinline__ void fft_dif(cplx *sbuf, int t, const cplx *__restrict__ tw,
+                                        GLoad &&gload, cplx (&out)[PL::V]) {
+  constexpr int RL = PL::Rlast;
+  auto reg_store = [&](int i, int j, int, cplx v) { out[i * RL + j] = v; };
+  if constexpr (PL::P == 1) {
+    dif_pass<PL, 0, INV>(t, tw, gload, reg_store);
+  } else {
+    auto s_load = [&](int pos) { return sbuf[swz(pos)]; };
+    auto s_store = [&](int, int, int pos, cplx v) { sbuf[swz(pos)] = v; };
+    __syncthreads();  // previous readers of sbuf are done
+    dif_pass<PL, 0, INV>(t, tw, gload, s_store);
+    sfor<PL::P - 2>([&](auto qc) {
+      constexpr int q = decltype(qc)::value + 1;
+      __syncthreads();
+      dif_pass<PL, q, INV>(t, tw, s_load, s_store);
+    });
+    __syncthreads();
+    dif_pass<PL, PL::P - 1, INV>(t, tw, s_load, reg_store);
+  }
+}
+
+// Final forward transform: digit-reversed registers -> natural order via gstore(pos, v).
+template <class PL, class GStore>
+__device__ __forceinline__ void fft_dit_final(cplx *sbuf, int t, const cplx *__restrict__ tw,
+                                              cplx (&in)[PL::V], GStore &&gstore) {
+  constexpr int RL = PL::Rlast;
+  auto reg_load = [&](int i, int j, int) { return in[i * RL + j]; };
+  auto g_store = [&](int, int, int pos, cplx v) { gstore(pos, v); };
+  if constexpr (PL::P == 1) {
+    dit_pass<PL, 0>(t, tw, reg_load, g_store);
+  } else {
+    auto s_load = [&](int, int, int pos) { return sbuf[swz(pos)]; };
+    auto s_store = [&](int, int, int pos, cplx v) { sbuf[swz(pos)] = v; };
+    __syncthreads();
+    dit_pass<PL, PL::P - 1>(t, tw, reg_load, s_store);
+    sfor<PL::P - 2>([&](auto qc) {
+      constexpr int q = PL::P - 2 - decltype(qc)::value;
+      __syncthreads();
+      dit_pass<PL, q>(t, tw, s_load, s_store);
+    });
+    __syncthreads();
+    dit_pass<PL, 0>(t, tw, s_load, g_store);
+  }
+}
+
+}  // namespace hk

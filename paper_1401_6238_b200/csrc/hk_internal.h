@@ -1,0 +1,59 @@
+// Internal (non-exported) declarations shared by the CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hk {
+
+// How one factor of the spectral product is supplied.
+enum FactorKind : int32_t {
+  FK_C128 = 0,  // complex128 vector, zero-padded to L and transformed in-kernel
+  FK_F64 = 1,   // float64 vector (imaginary part zero), zero-padded and transformed
+  FK_SPEC = 2,  // precomputed spectrum in the kernel's internal layout (length L)
+};
+
+enum Mode1D : int32_t {
+  M_PARTIAL = 0,  // y = fft(S .* prod X)[:out_len]           (hankel.py:42-45,140-147)
+  M_FULL = 1,     // alpha = sum(S .* prod X)                 (hankel.py:47-59,149-154)
+  M_SPEC_H = 2,   // write S = ifft(h) in internal layout     (hankel.py:37-40)
+  M_SPEC_F = 3,   // write X = fft(fac[0]) in internal layout (column spectra, K5)
+};
+
+// Batch index q of a launch splits as q = b * nsub + s; item (b, s) of a
+// factor starts at ptr + b * bstride + s * sstride elements, and vector entry
+// k sits at + k * estride.
+struct Factor {
+  const void *ptr;
+  long long bstride;
+  long long sstride;
+  int32_t len;       // nonzero prefix length; positions >= len are zero
+  int32_t power;     // multiplicity in the product
+  int32_t kind;      // FactorKind
+  int32_t estride;   // element stride inside one vector (1 = contiguous)
+};
+
+constexpr int kMaxFactors = 32;
+
+struct Args1D {
+  Factor h;                 // generating vector (inverse transform) or cached spectrum
+  Factor fac[kMaxFactors];  // distinct vector factors
+  int32_t nfac;
+  int32_t mode;
+  void *out;                // complex128 output, same (b, s) addressing as factors
+  long long out_bstride;
+  long long out_sstride;
+  int32_t out_len;          // number of outputs kept (n_1) for M_PARTIAL
+  int32_t out_estride;      // element stride of y
+  long long batch;          // total launch items (= outer * nsub)
+  long long nsub;           // >= 1
+  const double2 *tw;        // W_L^e, e in [0, L)
+  double scale;             // 1/L for the inverse transform
+};
+
+// Launch the fused 1D kernel for FFT length L (must be supported).
+cudaError_t launch_1d(int L, const Args1D &a, cudaStream_t stream);
+bool supported_1d(long long L);
+long long choose_len_1d(long long d);  // smallest supported on-chip L >= d, or -1
+
+}  // namespace hk
