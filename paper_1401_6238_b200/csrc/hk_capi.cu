@@ -1,6 +1,7 @@
 // C ABI implementation (include/hankelfft_b200.h): plans, twiddle tables,
 // validation, operand de-duplication and kernel dispatch.
 #include <math.h>
+#include <stdlib.h>
 
 #include <map>
 #include <mutex>
@@ -26,11 +27,13 @@ struct hk_plan {
   std::vector<int64_t> dof;     // per level: sum - m + 1
   std::vector<int64_t> L;       // per level FFT length
   const double2 *tw = nullptr;  // 1D twiddle table (length L[0])
+  const double2 *tw0 = nullptr; // thread-major first-pass table for the fast kernels
 };
 
 namespace {
 
 thread_local std::string g_err;
+bool g_force_generic = getenv("HK_FORCE_GENERIC") != nullptr;  // A/B switch for tests
 
 int fail(int code, const char *fmt, ...) {
   char buf[512];
@@ -83,6 +86,46 @@ int get_twiddles(int device, long long L, const double2 **out) {
   return HK_OK;
 }
 
+// Thread-major first-pass twiddles: T0[(j-1) * (L/R0) + b] = W_L^{j b}.
+std::map<std::pair<int, long long>, double2 *> g_tw0;
+
+int get_twiddles0(int device, long long L, int R0, const double2 **out) {
+  std::lock_guard<std::mutex> lk(g_tw_mu);
+  auto key = std::make_pair(device, L);
+  auto it = g_tw0.find(key);
+  if (it != g_tw0.end()) {
+    *out = it->second;
+    return HK_OK;
+  }
+  const long long nb = L / R0;
+  std::vector<double2> host((R0 - 1) * nb);
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  for (int j = 1; j < R0; ++j)
+    for (long long b = 0; b < nb; ++b) {
+      long long e = (j * b) % L;
+      long double ang = two_pi * (long double)e / (long double)L;
+      double2 w;
+      w.x = (double)cosl(ang);
+      w.y = (double)-sinl(ang);
+      if (4 * e == L) w = make_double2(0.0, -1.0);
+      if (2 * e == L) w = make_double2(-1.0, 0.0);
+      if (4 * e == 3 * L) w = make_double2(0.0, 1.0);
+      if (e == 0) w = make_double2(1.0, 0.0);
+      host[(j - 1) * nb + b] = w;
+    }
+  double2 *d = nullptr;
+  cudaError_t err = cudaMalloc(&d, host.size() * sizeof(double2));
+  if (err != cudaSuccess) return cuda_fail(err, "cudaMalloc(twiddles0)");
+  err = cudaMemcpy(d, host.data(), host.size() * sizeof(double2), cudaMemcpyHostToDevice);
+  if (err != cudaSuccess) {
+    cudaFree(d);
+    return cuda_fail(err, "cudaMemcpy(twiddles0)");
+  }
+  g_tw0[key] = d;
+  *out = d;
+  return HK_OK;
+}
+
 int check_plan(const hk_plan *p) {
   if (!p) return fail(HK_EINVAL, "plan is NULL");
   int dev = -1;
@@ -119,6 +162,7 @@ Args1D base_args(const hk_plan *p, int64_t batch) {
   a.batch = batch;
   a.nsub = 1;
   a.tw = p->tw;
+  a.tw0 = p->tw0;
   a.scale = 1.0 / (double)p->L[0];
   a.out_estride = 1;
   return a;
@@ -163,7 +207,9 @@ int set_vectors(const hk_plan *p, const hk_operand *xs, int nx, int mode_offset,
 }
 
 int launch(const hk_plan *p, const Args1D &a, void *stream) {
-  cudaError_t e = hk::launch_1d((int)p->L[0], a, (cudaStream_t)stream);
+  cudaError_t e = cudaErrorNotSupported;
+  if (!g_force_generic) e = hk::launch_fast_1d((int)p->L[0], a, (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported) e = hk::launch_1d((int)p->L[0], a, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "hankel 1d kernel launch");
   return HK_OK;
 }
@@ -204,6 +250,8 @@ int hk_plan_create_hankel(hk_plan **plan, int order, const int64_t *mode_sizes, 
   p->dof = {d};
   p->L = {L};
   int rc = get_twiddles(dev, L, &p->tw);
+  const int r0 = hk::fast_first_radix(L);
+  if (!rc && r0 > 0) rc = get_twiddles0(dev, L, r0, &p->tw0);
   if (rc) {
     delete p;
     return rc;

@@ -226,3 +226,87 @@ struct Dft<8, INV> {
 };
 
 }  // namespace hk
+
+namespace hk {
+
+// ---------------------------------------------------------------- pruned codelets
+// DftP<R, INV, NZ, NO>: inputs v[n] are zero for n >= NZ (not read), and only
+// outputs v[k], k < NO, are produced (the rest are left undefined).  Used for
+// the zero-padded first pass of a vector transform (x has n << L nonzeros) and
+// the truncated last pass of the final transform (only y[:n_1] is kept).
+template <int R, bool INV, int NZ, int NO, bool Composite = (R > 4)>
+struct DftP;
+
+// small radices: full codelet when nothing is pruned, direct sums otherwise
+template <int R, bool INV, int NZ, int NO>
+struct DftP<R, INV, NZ, NO, false> {
+  __device__ __forceinline__ static void run(cplx *v) {
+    if constexpr (NZ >= R && NO >= R) {
+      Dft<R, INV>::run(v);
+    } else if constexpr (NZ == 1) {
+      sfor<NO>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        if constexpr (k > 0) v[k] = v[0];
+      });
+    } else {
+      cplx x[NZ];
+      sfor<NZ>([&](auto nc) { x[decltype(nc)::value] = v[decltype(nc)::value]; });
+      sfor<NO>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        cplx s = x[0];
+        sfor<NZ - 1>([&](auto nc) {
+          constexpr int n = decltype(nc)::value + 1;
+          s = cadd(s, twc<n * k, R, INV>(x[n]));
+        });
+        v[k] = s;
+      });
+    }
+  }
+};
+
+template <int R, bool INV, int NZ, int NO>
+struct DftP<R, INV, NZ, NO, true> {
+  static constexpr int R1 = first_factor(R);
+  static constexpr int R2 = R / R1;
+  static constexpr int NZ2 = NZ < R2 ? NZ : R2;  // nonzero n2 columns
+  static constexpr int NO1 = NO < R1 ? NO : R1;  // needed k1 rows
+  __device__ __forceinline__ static void run(cplx *v) {
+    if constexpr (NZ >= R && NO >= R) {
+      Dft<R, INV>::run(v);
+    } else {
+      cplx t[R];
+      sfor<NZ2>([&](auto n2c) {
+        constexpr int n2 = decltype(n2c)::value;
+        constexpr int nz1c = (NZ - n2 + R2 - 1) / R2;
+        constexpr int nz1 = nz1c > R1 ? R1 : nz1c;
+        cplx a[R1];
+        sfor<nz1>([&](auto n1c) {
+          constexpr int n1 = decltype(n1c)::value;
+          a[n1] = v[n1 * R2 + n2];
+        });
+        DftP<R1, INV, nz1, NO1>::run(a);
+        sfor<NO1>([&](auto k1c) {
+          constexpr int k1 = decltype(k1c)::value;
+          t[k1 * R2 + n2] = twc<n2 * k1, R, INV>(a[k1]);
+        });
+      });
+      sfor<NO1>([&](auto k1c) {
+        constexpr int k1 = decltype(k1c)::value;
+        constexpr int no2c = (NO - k1 + R1 - 1) / R1;
+        constexpr int no2 = no2c > R2 ? R2 : no2c;
+        cplx b[R2];
+        sfor<NZ2>([&](auto n2c) {
+          constexpr int n2 = decltype(n2c)::value;
+          b[n2] = t[k1 * R2 + n2];
+        });
+        DftP<R2, INV, NZ2, no2>::run(b);
+        sfor<no2>([&](auto k2c) {
+          constexpr int k2 = decltype(k2c)::value;
+          v[k1 + R1 * k2] = b[k2];
+        });
+      });
+    }
+  }
+};
+
+}  // namespace hk

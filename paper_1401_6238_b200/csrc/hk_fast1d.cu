@@ -1,0 +1,378 @@
+// K1/K2 fast path: fused batched 1D Hankel products with a TMEM-resident
+// spectral accumulator, pruned first/last passes and conflict-free,
+// low-traffic twiddle access.
+//
+// Per product (reference hankel.py:140-154 via hankel.py:42-71):
+//   acc  = ifft(h~)                        -> TMEM
+//   for each distinct vector factor f:     (H x^{m-1}: one factor, power m-1)
+//       X = fft(x~_f)   (first pass pruned to the n_f/s_0 nonzero inputs)
+//       acc = acc .* X .* ... .* X         (TMEM chunk by chunk; reference order)
+//   partial: y = fft(acc)[:n_1]            (transposed network, last pass pruned
+//                                           to the n_1/s_0 needed outputs)
+//   full:    alpha = sum(acc)              (fixed-order reduction)
+//
+// Differences from the generic kernel (hk_1d.cu):
+//  * acc lives in TMEM, so only one length-L working set is in registers:
+//    <= 128 registers/thread -> 2 CTAs (16 warps) per SM;
+//  * pass-0 twiddles come from a thread-major table (one coalesced 16 B load
+//    per value instead of a stride-j gather), middle passes map lanes onto the
+//    butterfly-group index so their twiddles are warp-uniform (broadcast);
+//  * the smem swizzle XORs the low 3 position bits with bits 4-6 ^ 8-10, which
+//    keeps every 8-lane phase of every pass on distinct 16 B bank groups.
+#include <atomic>
+
+#include "hk_fft1d.cuh"
+#include "hk_internal.h"
+#include "hk_tmem.cuh"
+
+namespace hk {
+namespace fast {
+
+__device__ __forceinline__ int swz2(int pos) { return pos ^ (((pos >> 4) ^ (pos >> 8)) & 7); }
+
+template <class PL>
+struct Traits {
+  static constexpr int hi_count(int p) { return PL::L / (PL::stride(p) * PL::radix[p]); }
+  static constexpr bool hi_major(int p) { return p > 0 && p < PL::P - 1 && hi_count(p) >= 8; }
+  static constexpr int warps = PL::CTA / 32;
+  static constexpr int slabs = (warps + 3) / 4;
+  static constexpr int cols_needed = slabs * 4 * PL::V;
+  static constexpr int tmem_cols = cols_needed <= 32    ? 32
+                                   : cols_needed <= 64  ? 64
+                                   : cols_needed <= 128 ? 128
+                                   : cols_needed <= 256 ? 256
+                                                        : 512;
+  static_assert(cols_needed <= 512, "accumulator does not fit in TMEM");
+  static_assert(PL::V % 4 == 0, "TMEM chunks of 4 complex values");
+  static constexpr int min_blocks = (PL::CTA <= 256) ? 2 : 1;
+};
+
+// One pass.  FINAL=false: DIF (butterfly then twiddle), pruned to NZ nonzero
+// inputs.  FINAL=true: transposed DIT of the forward transform (twiddle then
+// butterfly), pruned to NO needed outputs.
+template <class PL, int p, bool INV, bool FINAL, int NZ, int NO, class Load, class Store>
+__device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw,
+                                     const cplx *__restrict__ tw0, Load &&load, Store &&store) {
+  using Tr = Traits<PL>;
+  constexpr int R = PL::radix[p];
+  constexpr int s = PL::stride(p);
+  constexpr int Lp = s * R;
+  constexpr int NBUT = PL::L / R;
+  constexpr int NB = (NBUT + PL::T - 1) / PL::T;
+  constexpr int H = Tr::hi_count(p);
+  constexpr bool HIM = Tr::hi_major(p);
+  constexpr int NIN = FINAL ? R : NZ;
+  constexpr int NOUT = FINAL ? NO : R;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    const int beta = t + i * PL::T;
+    if (NBUT % PL::T == 0 || beta < NBUT) {
+      int lo, hi;
+      if constexpr (HIM) {
+        hi = beta % H;
+        lo = beta / H;
+      } else {
+        lo = beta % s;
+        hi = beta / s;
+      }
+      const int base = hi * Lp + lo;
+      cplx a[R];
+      sfor<NIN>([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
+        a[j] = load(i, j, base + j * s);
+      });
+      auto twiddle = [&]() {
+        if constexpr (p < PL::P - 1) {
+          sfor<R>([&](auto jc) {
+            constexpr int j = decltype(jc)::value;
+            if constexpr (j > 0) {
+              cplx w;
+              if constexpr (p == 0) {
+                w = __ldg(&tw0[(j - 1) * NBUT + beta]);
+              } else {
+                w = __ldg(&tw[j * lo * (PL::L / Lp)]);
+              }
+              a[j] = cmul_dir<INV>(a[j], w);
+            }
+          });
+        }
+      };
+      if constexpr (FINAL) {
+        twiddle();
+        DftP<R, false, R, NO>::run(a);
+      } else {
+        DftP<R, INV, NZ, R>::run(a);
+        twiddle();
+      }
+      sfor<NOUT>([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
+        store(i, j, base + j * s, a[j]);
+      });
+    }
+  }
+}
+
+template <class PL, bool INV, int NZ, class GLoad>
+__device__ __forceinline__ void fft_dif(cplx *sbuf, int t, const cplx *__restrict__ tw,
+                                        const cplx *__restrict__ tw0, GLoad &&gload,
+                                        cplx (&out)[PL::V]) {
+  constexpr int RL = PL::Rlast;
+  constexpr int R0 = PL::radix[0];
+  auto g_load = [&](int, int, int pos) { return gload(pos); };
+  auto s_load = [&](int, int, int pos) { return sbuf[swz2(pos)]; };
+  auto s_store = [&](int, int, int pos, cplx v) { sbuf[swz2(pos)] = v; };
+  auto r_store = [&](int i, int j, int, cplx v) { out[i * RL + j] = v; };
+  static_assert(PL::P >= 2, "fast path needs at least two passes");
+  __syncthreads();
+  pass<PL, 0, INV, false, (NZ < R0 ? NZ : R0), R0>(t, tw, tw0, g_load, s_store);
+  sfor<PL::P - 2>([&](auto qc) {
+    constexpr int q = decltype(qc)::value + 1;
+    __syncthreads();
+    pass<PL, q, INV, false, PL::radix[q], PL::radix[q]>(t, tw, tw0, s_load, s_store);
+  });
+  __syncthreads();
+  pass<PL, PL::P - 1, INV, false, RL, RL>(t, tw, tw0, s_load, r_store);
+}
+
+template <class PL, int NO, class GStore>
+__device__ __forceinline__ void fft_final(cplx *sbuf, int t, const cplx *__restrict__ tw,
+                                          const cplx *__restrict__ tw0, cplx (&in)[PL::V],
+                                          GStore &&gstore) {
+  constexpr int RL = PL::Rlast;
+  constexpr int R0 = PL::radix[0];
+  auto r_load = [&](int i, int j, int) { return in[i * RL + j]; };
+  auto s_load = [&](int, int, int pos) { return sbuf[swz2(pos)]; };
+  auto s_store = [&](int, int, int pos, cplx v) { sbuf[swz2(pos)] = v; };
+  auto g_store = [&](int, int, int pos, cplx v) { gstore(pos, v); };
+  __syncthreads();
+  pass<PL, PL::P - 1, false, true, RL, RL>(t, tw, tw0, r_load, s_store);
+  sfor<PL::P - 2>([&](auto qc) {
+    constexpr int q = PL::P - 2 - decltype(qc)::value;
+    __syncthreads();
+    pass<PL, q, false, true, PL::radix[q], PL::radix[q]>(t, tw, tw0, s_load, s_store);
+  });
+  __syncthreads();
+  pass<PL, 0, false, true, R0, (NO < R0 ? NO : R0)>(t, tw, tw0, s_load, g_store);
+}
+
+__device__ __forceinline__ cplx load_elem(const Factor &f, long long off, int pos, double scale) {
+  if (pos >= f.len) return make_double2(0.0, 0.0);
+  const long long k = (long long)pos * f.estride;
+  if (f.kind == FK_F64) {
+    const double *p = static_cast<const double *>(f.ptr) + off;
+    return make_double2(__ldg(p + k) * scale, 0.0);
+  }
+  const cplx *p = static_cast<const cplx *>(f.ptr) + off;
+  cplx v = __ldg(p + k);
+  return make_double2(v.x * scale, v.y * scale);
+}
+
+template <class PL, int NZ, int NO>
+__global__ void __launch_bounds__(PL::CTA, Traits<PL>::min_blocks)
+    k_hankel_fast(const __grid_constant__ Args1D a) {
+  using Tr = Traits<PL>;
+  constexpr int T = PL::T;
+  constexpr int V = PL::V;
+  constexpr int COLS = Tr::tmem_cols;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint32_t tmem_slot;
+  cplx *smem = reinterpret_cast<cplx *>(smem_raw);
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc<COLS>(&tmem_slot);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tbase = tmem_slot;
+  const uint32_t tmy = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 4 * V);
+
+  const int g = threadIdx.x / T;
+  const int t = threadIdx.x - g * T;
+  long long b = (long long)blockIdx.x * PL::G + g;
+  const bool active = b < a.batch;
+  if (!active) b = a.batch - 1;
+  const long long ob = b / a.nsub, os = b - ob * a.nsub;
+  cplx *sbuf = smem + g * PL::L;
+  const cplx *__restrict__ tw = a.tw;
+  const cplx *__restrict__ tw0 = a.tw0;
+
+  cplx v[V];
+  // ---- acc = ifft(h~) (or cached spectrum) -> TMEM
+  {
+    const Factor &hf = a.h;
+    const long long off = ob * hf.bstride + os * hf.sstride;
+    if (hf.kind == FK_SPEC) {
+      const cplx *sp = static_cast<const cplx *>(hf.ptr) + off;
+#pragma unroll
+      for (int r = 0; r < V; ++r) v[r] = __ldg(sp + r * T + t);
+    } else {
+      const double sc = a.scale;
+      fft_dif<PL, true, PL::radix[0]>(sbuf, t, tw, tw0,
+                                       [&](int pos) { return load_elem(hf, off, pos, sc); }, v);
+    }
+#pragma unroll
+    for (int c = 0; c < V / 4; ++c) tmem_st4(tmy + 16 * c, &v[4 * c]);
+  }
+  // ---- acc .*= fft(x~_f)^{p_f}
+  for (int f = 0; f < a.nfac; ++f) {
+    const Factor &fa = a.fac[f];
+    const long long off = ob * fa.bstride + os * fa.sstride;
+    if (fa.kind == FK_SPEC) {
+      const cplx *sp = static_cast<const cplx *>(fa.ptr) + off;
+#pragma unroll
+      for (int r = 0; r < V; ++r) v[r] = __ldg(sp + r * T + t);
+    } else {
+      fft_dif<PL, false, NZ>(sbuf, t, tw, tw0,
+                             [&](int pos) { return load_elem(fa, off, pos, 1.0); }, v);
+    }
+    tmem_wait_st();
+#pragma unroll
+    for (int c = 0; c < V / 4; ++c) {
+      cplx acc[4];
+      tmem_ld4(tmy + 16 * c, acc);
+      for (int k = 0; k < fa.power; ++k) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] = cmul(acc[q], v[4 * c + q]);
+      }
+      tmem_st4(tmy + 16 * c, acc);
+    }
+  }
+  tmem_wait_st();
+#pragma unroll
+  for (int c = 0; c < V / 4; ++c) tmem_ld4(tmy + 16 * c, &v[4 * c]);
+
+  cplx *out = static_cast<cplx *>(a.out) + ob * a.out_bstride + os * a.out_sstride;
+  if (a.mode == M_PARTIAL) {
+    const int n1 = a.out_len;
+    const long long es = a.out_estride;
+    fft_final<PL, NO>(sbuf, t, tw, tw0, v, [&](int pos, cplx val) {
+      if (active && pos < n1) out[pos * es] = val;
+    });
+  } else {
+    cplx s = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < V; ++r) s = cadd(s, v[r]);
+    __syncthreads();
+    cplx *red = smem + g * T;
+    red[t] = s;
+    __syncthreads();
+    if (t == 0 && active) {
+      cplx tot = make_double2(0.0, 0.0);
+      for (int k = 0; k < T; ++k) tot = cadd(tot, red[k]);
+      out[0] = tot;
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tmem_fence_after();
+    tmem_dealloc<COLS>(tbase);
+  }
+}
+
+template <class PL, int NZ, int NO>
+static cudaError_t launch_variant(const Args1D &a, cudaStream_t stream) {
+  const int smem = PL::G * PL::L * (int)sizeof(cplx);
+  static std::atomic<unsigned long long> configured{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(configured.load() & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(k_hankel_fast<PL, NZ, NO>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured.fetch_or(bit);
+  }
+  const long long grid = (a.batch + PL::G - 1) / PL::G;
+  if (grid <= 0) return cudaSuccess;
+  k_hankel_fast<PL, NZ, NO><<<(unsigned)grid, PL::CTA, smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+// Choose the smallest instantiated pruning level covering the request.
+template <int I, int N, class F>
+static void hfor_impl(F &&f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    hfor_impl<I + 1, N>(f);
+  }
+}
+template <int N, class F>
+static void hfor(F &&f) { hfor_impl<0, N>(f); }
+
+template <class PL, int... Ls>
+struct Pruned {
+  static constexpr int n = sizeof...(Ls);
+  static constexpr int lv[n] = {Ls...};
+  static int pick(int want) {
+    for (int i = 0; i < n; ++i)
+      if (want <= lv[i]) return i;
+    return n - 1;
+  }
+  static cudaError_t launch(const Args1D &a, cudaStream_t stream, int nz, int no) {
+    const int zi = pick(nz), oi = pick(no);
+    cudaError_t r = cudaErrorInvalidValue;
+    hfor<n>([&](auto zc) {
+      hfor<n>([&](auto oc) {
+        constexpr int Z = decltype(zc)::value, O = decltype(oc)::value;
+        if (Z == zi && O == oi) r = launch_variant<PL, lv[Z], lv[O]>(a, stream);
+      });
+    });
+    return r;
+  }
+};
+
+}  // namespace fast
+
+// Fast-path dispatch; returns cudaErrorNotSupported when L has no fast variant
+// or the request needs a mode the fast kernel does not implement.
+int fast_first_radix(long long L) {
+  switch (L) {
+    case 4096: return 16;
+    case 6144: return 24;
+    case 2048: return 8;
+    case 1024: return 4;
+    case 512: return 2;
+    case 256: return 16;
+    case 8192: return 2;
+    default: return 0;
+  }
+}
+
+cudaError_t launch_fast_1d(int L, const Args1D &a, cudaStream_t stream) {
+  if (a.mode != M_PARTIAL && a.mode != M_FULL) return cudaErrorNotSupported;
+  if (!a.tw0) return cudaErrorNotSupported;
+  int maxlen = 1;
+  for (int f = 0; f < a.nfac; ++f)
+    if (a.fac[f].kind != FK_SPEC && a.fac[f].len > maxlen) maxlen = a.fac[f].len;
+  const int outl = a.mode == M_PARTIAL ? a.out_len : L;
+  switch (L) {
+    case 4096: {
+      using PL = Plan1D<4096, 256, 16, 16, 16>;
+      const int s0 = PL::stride(0);
+      return fast::Pruned<PL, 4, 8, 16>::launch(a, stream, (maxlen + s0 - 1) / s0,
+                                                (outl + s0 - 1) / s0);
+    }
+    case 6144: {
+      using PL = Plan1D<6144, 384, 24, 16, 16>;
+      const int s0 = PL::stride(0);
+      return fast::Pruned<PL, 8, 12, 24>::launch(a, stream, (maxlen + s0 - 1) / s0,
+                                                 (outl + s0 - 1) / s0);
+    }
+    case 2048:
+      return fast::launch_variant<Plan1D<2048, 128, 8, 16, 16>, 8, 8>(a, stream);
+    case 1024:
+      return fast::launch_variant<Plan1D<1024, 64, 4, 16, 16>, 4, 4>(a, stream);
+    case 512:
+      return fast::launch_variant<Plan1D<512, 32, 2, 16, 16>, 2, 2>(a, stream);
+    case 256:
+      return fast::launch_variant<Plan1D<256, 16, 16, 16>, 16, 16>(a, stream);
+    case 8192: {
+      using PL = Plan1D<8192, 512, 2, 16, 16, 16>;
+      return fast::launch_variant<PL, 2, 2>(a, stream);
+    }
+    default:
+      return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace hk

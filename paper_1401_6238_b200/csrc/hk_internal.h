@@ -48,12 +48,16 @@ struct Args1D {
   long long batch;          // total launch items (= outer * nsub)
   long long nsub;           // >= 1
   const double2 *tw;        // W_L^e, e in [0, L)
+  const double2 *tw0;       // thread-major first-pass table (fast path), may be NULL
   double scale;             // 1/L for the inverse transform
 };
 
 // Launch the fused 1D kernel for FFT length L (must be supported).
 cudaError_t launch_1d(int L, const Args1D &a, cudaStream_t stream);
 bool supported_1d(long long L);
+// Fast path (hk_fast1d.cu): cudaErrorNotSupported if not applicable.
+cudaError_t launch_fast_1d(int L, const Args1D &a, cudaStream_t stream);
+int fast_first_radix(long long L);  // R_0 of the fast plan, 0 if none
 long long choose_len_1d(long long d);  // smallest supported on-chip L >= d, or -1
 
 }  // namespace hk
