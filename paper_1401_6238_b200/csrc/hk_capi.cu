@@ -165,6 +165,7 @@ Args1D base_args(const hk_plan *p, int64_t batch) {
   a.tw0 = p->tw0;
   a.scale = 1.0 / (double)p->L[0];
   a.out_estride = 1;
+  a.prefetch = getenv("HK_NO_PREFETCH") ? 0 : 1;
   return a;
 }
 

@@ -20,6 +20,8 @@
 //  * the smem swizzle XORs the low 3 position bits with bits 4-6 ^ 8-10, which
 //    keeps every 8-lane phase of every pass on distinct 16 B bank groups.
 #include <atomic>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "hk_fft1d.cuh"
 #include "hk_internal.h"
@@ -167,6 +169,30 @@ __device__ __forceinline__ cplx load_elem(const Factor &f, long long off, int po
   return make_double2(v.x * scale, v.y * scale);
 }
 
+// L2 prefetch (cp.async.bulk.prefetch.L2) of one operand item, if contiguous.
+__device__ __forceinline__ void prefetch_item(const Factor &f, long long b, long long nsub,
+                                              int kind_bytes) {
+  if (f.kind == FK_SPEC || f.estride != 1 || f.len <= 0) return;
+  const long long ob = b / nsub, os = b - ob * nsub;
+  const char *p = static_cast<const char *>(f.ptr) + (ob * f.bstride + os * f.sstride) * kind_bytes;
+  unsigned bytes = (unsigned)f.len * (unsigned)kind_bytes;
+  // 16-byte aligned start and size
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+  const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~(uintptr_t)15;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a0), "r"((unsigned)(a1 - a0))
+               : "memory");
+}
+
+__device__ __forceinline__ void prefetch_block(const Args1D &a, long long bb, int G) {
+  for (int g = 0; g < G; ++g) {
+    const long long b = bb * G + g;
+    if (b >= a.batch) break;
+    prefetch_item(a.h, b, a.nsub, a.h.kind == FK_F64 ? 8 : 16);
+    for (int f = 0; f < a.nfac; ++f)
+      prefetch_item(a.fac[f], b, a.nsub, a.fac[f].kind == FK_F64 ? 8 : 16);
+  }
+}
+
 template <class PL, int NZ, int NO>
 __global__ void __launch_bounds__(PL::CTA, Traits<PL>::min_blocks)
     k_hankel_fast(const __grid_constant__ Args1D a) {
@@ -187,78 +213,88 @@ __global__ void __launch_bounds__(PL::CTA, Traits<PL>::min_blocks)
 
   const int g = threadIdx.x / T;
   const int t = threadIdx.x - g * T;
-  long long b = (long long)blockIdx.x * PL::G + g;
-  const bool active = b < a.batch;
-  if (!active) b = a.batch - 1;
-  const long long ob = b / a.nsub, os = b - ob * a.nsub;
+  const long long nblk = (a.batch + PL::G - 1) / PL::G;
   cplx *sbuf = smem + g * PL::L;
   const cplx *__restrict__ tw = a.tw;
   const cplx *__restrict__ tw0 = a.tw0;
+  const bool do_pf = a.prefetch != 0;
+  if (do_pf && threadIdx.x == 0) prefetch_block(a, blockIdx.x, PL::G);
 
-  cplx v[V];
-  // ---- acc = ifft(h~) (or cached spectrum) -> TMEM
-  {
-    const Factor &hf = a.h;
-    const long long off = ob * hf.bstride + os * hf.sstride;
-    if (hf.kind == FK_SPEC) {
-      const cplx *sp = static_cast<const cplx *>(hf.ptr) + off;
+  // persistent loop: block bb handles products bb*G .. bb*G+G-1
+  for (long long bb = blockIdx.x; bb < nblk; bb += gridDim.x) {
+    // stream the NEXT block's inputs into L2 while this one computes
+    if (do_pf && threadIdx.x == 0 && bb + gridDim.x < nblk) prefetch_block(a, bb + gridDim.x, PL::G);
+    long long b = bb * PL::G + g;
+    const bool active = b < a.batch;
+    if (!active) b = a.batch - 1;
+    const long long ob = b / a.nsub, os = b - ob * a.nsub;
+
+    cplx v[V];
+    // ---- acc = ifft(h~) (or cached spectrum) -> TMEM
+    {
+      const Factor &hf = a.h;
+      const long long off = ob * hf.bstride + os * hf.sstride;
+      if (hf.kind == FK_SPEC) {
+        const cplx *sp = static_cast<const cplx *>(hf.ptr) + off;
 #pragma unroll
-      for (int r = 0; r < V; ++r) v[r] = __ldg(sp + r * T + t);
-    } else {
-      const double sc = a.scale;
-      fft_dif<PL, true, PL::radix[0]>(sbuf, t, tw, tw0,
-                                       [&](int pos) { return load_elem(hf, off, pos, sc); }, v);
+        for (int r = 0; r < V; ++r) v[r] = __ldg(sp + r * T + t);
+      } else {
+        const double sc = a.scale;
+        fft_dif<PL, true, PL::radix[0]>(
+            sbuf, t, tw, tw0, [&](int pos) { return load_elem(hf, off, pos, sc); }, v);
+      }
+      tmem_wait_st();  // previous product's final reads of TMEM are complete
+#pragma unroll
+      for (int c = 0; c < V / 4; ++c) tmem_st4(tmy + 16 * c, &v[4 * c]);
     }
+    // ---- acc .*= fft(x~_f)^{p_f}
+    for (int f = 0; f < a.nfac; ++f) {
+      const Factor &fa = a.fac[f];
+      const long long off = ob * fa.bstride + os * fa.sstride;
+      if (fa.kind == FK_SPEC) {
+        const cplx *sp = static_cast<const cplx *>(fa.ptr) + off;
 #pragma unroll
-    for (int c = 0; c < V / 4; ++c) tmem_st4(tmy + 16 * c, &v[4 * c]);
-  }
-  // ---- acc .*= fft(x~_f)^{p_f}
-  for (int f = 0; f < a.nfac; ++f) {
-    const Factor &fa = a.fac[f];
-    const long long off = ob * fa.bstride + os * fa.sstride;
-    if (fa.kind == FK_SPEC) {
-      const cplx *sp = static_cast<const cplx *>(fa.ptr) + off;
+        for (int r = 0; r < V; ++r) v[r] = __ldg(sp + r * T + t);
+      } else {
+        fft_dif<PL, false, NZ>(sbuf, t, tw, tw0,
+                               [&](int pos) { return load_elem(fa, off, pos, 1.0); }, v);
+      }
+      tmem_wait_st();
 #pragma unroll
-      for (int r = 0; r < V; ++r) v[r] = __ldg(sp + r * T + t);
-    } else {
-      fft_dif<PL, false, NZ>(sbuf, t, tw, tw0,
-                             [&](int pos) { return load_elem(fa, off, pos, 1.0); }, v);
+      for (int c = 0; c < V / 4; ++c) {
+        cplx acc[4];
+        tmem_ld4(tmy + 16 * c, acc);
+        for (int k = 0; k < fa.power; ++k) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q] = cmul(acc[q], v[4 * c + q]);
+        }
+        tmem_st4(tmy + 16 * c, acc);
+      }
     }
     tmem_wait_st();
 #pragma unroll
-    for (int c = 0; c < V / 4; ++c) {
-      cplx acc[4];
-      tmem_ld4(tmy + 16 * c, acc);
-      for (int k = 0; k < fa.power; ++k) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[q] = cmul(acc[q], v[4 * c + q]);
-      }
-      tmem_st4(tmy + 16 * c, acc);
-    }
-  }
-  tmem_wait_st();
-#pragma unroll
-  for (int c = 0; c < V / 4; ++c) tmem_ld4(tmy + 16 * c, &v[4 * c]);
+    for (int c = 0; c < V / 4; ++c) tmem_ld4(tmy + 16 * c, &v[4 * c]);
 
-  cplx *out = static_cast<cplx *>(a.out) + ob * a.out_bstride + os * a.out_sstride;
-  if (a.mode == M_PARTIAL) {
-    const int n1 = a.out_len;
-    const long long es = a.out_estride;
-    fft_final<PL, NO>(sbuf, t, tw, tw0, v, [&](int pos, cplx val) {
-      if (active && pos < n1) out[pos * es] = val;
-    });
-  } else {
-    cplx s = make_double2(0.0, 0.0);
+    cplx *out = static_cast<cplx *>(a.out) + ob * a.out_bstride + os * a.out_sstride;
+    if (a.mode == M_PARTIAL) {
+      const int n1 = a.out_len;
+      const long long es = a.out_estride;
+      fft_final<PL, NO>(sbuf, t, tw, tw0, v, [&](int pos, cplx val) {
+        if (active && pos < n1) out[pos * es] = val;
+      });
+    } else {
+      cplx s = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int r = 0; r < V; ++r) s = cadd(s, v[r]);
-    __syncthreads();
-    cplx *red = smem + g * T;
-    red[t] = s;
-    __syncthreads();
-    if (t == 0 && active) {
-      cplx tot = make_double2(0.0, 0.0);
-      for (int k = 0; k < T; ++k) tot = cadd(tot, red[k]);
-      out[0] = tot;
+      for (int r = 0; r < V; ++r) s = cadd(s, v[r]);
+      __syncthreads();
+      cplx *red = smem + g * T;
+      red[t] = s;
+      __syncthreads();
+      if (t == 0 && active) {
+        cplx tot = make_double2(0.0, 0.0);
+        for (int k = 0; k < T; ++k) tot = cadd(tot, red[k]);
+        out[0] = tot;
+      }
     }
   }
   tmem_fence_before();
@@ -280,10 +316,44 @@ static cudaError_t launch_variant(const Args1D &a, cudaStream_t stream) {
     cudaError_t e = cudaFuncSetAttribute(k_hankel_fast<PL, NZ, NO>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
+    // Carve out just enough shared memory for the target residency; the rest
+    // stays L1 for the twiddle tables.
+    const int want = Traits<PL>::min_blocks * (smem + 2048);
+    const int pct = (want * 100 + 228 * 1024 - 1) / (228 * 1024);
+    e = cudaFuncSetAttribute(k_hankel_fast<PL, NZ, NO>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
+    if (e != cudaSuccess) return e;
     configured.fetch_or(bit);
   }
-  const long long grid = (a.batch + PL::G - 1) / PL::G;
-  if (grid <= 0) return cudaSuccess;
+  const long long nblk = (a.batch + PL::G - 1) / PL::G;
+  if (nblk <= 0) return cudaSuccess;
+  static int resident[64] = {0};
+  int &res = resident[dev & 63];
+  if (res == 0) {
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hankel_fast<PL, NZ, NO>, PL::CTA,
+                                                  smem);
+    // The occupancy API under-reports here; derive residency from the limits.
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_hankel_fast<PL, NZ, NO>);
+    int smem_sm = 0, regs_sm = 0;
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+    const int by_regs = regs_sm / (((fa.numRegs + 7) / 8 * 8) * PL::CTA);
+    const int by_smem = smem_sm / (smem + (int)fa.sharedSizeBytes + 1024);
+    const int by_thr = 2048 / PL::CTA;
+    int mine = by_regs < by_smem ? by_regs : by_smem;
+    mine = mine < by_thr ? mine : by_thr;
+    if (mine > per_sm) per_sm = mine;
+    res = sms * (per_sm > 0 ? per_sm : 1);
+    if (const char *e = getenv("HK_DEBUG_GRID")) {
+      fprintf(stderr, "[hk] fast L=%d sms=%d per_sm=%d grid=%d smem=%d\n", PL::L, sms, per_sm,
+              res, smem);
+      if (atoi(e) > 0) res = atoi(e);
+    }
+  }
+  const long long grid = nblk < res ? nblk : res;
   k_hankel_fast<PL, NZ, NO><<<(unsigned)grid, PL::CTA, smem, stream>>>(a);
   return cudaGetLastError();
 }

@@ -50,6 +50,8 @@ struct Args1D {
   const double2 *tw;        // W_L^e, e in [0, L)
   const double2 *tw0;       // thread-major first-pass table (fast path), may be NULL
   double scale;             // 1/L for the inverse transform
+  int32_t prefetch;         // fast path: L2-prefetch the next block's operands
+  int32_t pad2;
 };
 
 // Launch the fused 1D kernel for FFT length L (must be supported).
