@@ -209,7 +209,9 @@ int set_vectors(const hk_plan *p, const hk_operand *xs, int nx, int mode_offset,
 
 int launch(const hk_plan *p, const Args1D &a, void *stream) {
   cudaError_t e = cudaErrorNotSupported;
-  if (!g_force_generic) e = hk::launch_fast_1d((int)p->L[0], a, (cudaStream_t)stream);
+  if (!g_force_generic) e = hk::launch_pp_1d((int)p->L[0], a, (cudaStream_t)stream);
+  if (!g_force_generic && e == cudaErrorNotSupported)
+    e = hk::launch_fast_1d((int)p->L[0], a, (cudaStream_t)stream);
   if (e == cudaErrorNotSupported) e = hk::launch_1d((int)p->L[0], a, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "hankel 1d kernel launch");
   return HK_OK;

@@ -23,151 +23,10 @@
 #include <stdio.h>
 #include <stdlib.h>
 
-#include "hk_fft1d.cuh"
-#include "hk_internal.h"
-#include "hk_tmem.cuh"
+#include "hk_fastcore.cuh"
 
 namespace hk {
 namespace fast {
-
-__device__ __forceinline__ int swz2(int pos) { return pos ^ (((pos >> 4) ^ (pos >> 8)) & 7); }
-
-template <class PL>
-struct Traits {
-  static constexpr int hi_count(int p) { return PL::L / (PL::stride(p) * PL::radix[p]); }
-  static constexpr bool hi_major(int p) { return p > 0 && p < PL::P - 1 && hi_count(p) >= 8; }
-  static constexpr int warps = PL::CTA / 32;
-  static constexpr int slabs = (warps + 3) / 4;
-  static constexpr int cols_needed = slabs * 4 * PL::V;
-  static constexpr int tmem_cols = cols_needed <= 32    ? 32
-                                   : cols_needed <= 64  ? 64
-                                   : cols_needed <= 128 ? 128
-                                   : cols_needed <= 256 ? 256
-                                                        : 512;
-  static_assert(cols_needed <= 512, "accumulator does not fit in TMEM");
-  static_assert(PL::V % 4 == 0, "TMEM chunks of 4 complex values");
-  static constexpr int min_blocks = (PL::CTA <= 256) ? 2 : 1;
-};
-
-// One pass.  FINAL=false: DIF (butterfly then twiddle), pruned to NZ nonzero
-// inputs.  FINAL=true: transposed DIT of the forward transform (twiddle then
-// butterfly), pruned to NO needed outputs.
-template <class PL, int p, bool INV, bool FINAL, int NZ, int NO, class Load, class Store>
-__device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw,
-                                     const cplx *__restrict__ tw0, Load &&load, Store &&store) {
-  using Tr = Traits<PL>;
-  constexpr int R = PL::radix[p];
-  constexpr int s = PL::stride(p);
-  constexpr int Lp = s * R;
-  constexpr int NBUT = PL::L / R;
-  constexpr int NB = (NBUT + PL::T - 1) / PL::T;
-  constexpr int H = Tr::hi_count(p);
-  constexpr bool HIM = Tr::hi_major(p);
-  constexpr int NIN = FINAL ? R : NZ;
-  constexpr int NOUT = FINAL ? NO : R;
-#pragma unroll
-  for (int i = 0; i < NB; ++i) {
-    const int beta = t + i * PL::T;
-    if (NBUT % PL::T == 0 || beta < NBUT) {
-      int lo, hi;
-      if constexpr (HIM) {
-        hi = beta % H;
-        lo = beta / H;
-      } else {
-        lo = beta % s;
-        hi = beta / s;
-      }
-      const int base = hi * Lp + lo;
-      cplx a[R];
-      sfor<NIN>([&](auto jc) {
-        constexpr int j = decltype(jc)::value;
-        a[j] = load(i, j, base + j * s);
-      });
-      auto twiddle = [&]() {
-        if constexpr (p < PL::P - 1) {
-          sfor<R>([&](auto jc) {
-            constexpr int j = decltype(jc)::value;
-            if constexpr (j > 0) {
-              cplx w;
-              if constexpr (p == 0) {
-                w = __ldg(&tw0[(j - 1) * NBUT + beta]);
-              } else {
-                w = __ldg(&tw[j * lo * (PL::L / Lp)]);
-              }
-              a[j] = cmul_dir<INV>(a[j], w);
-            }
-          });
-        }
-      };
-      if constexpr (FINAL) {
-        twiddle();
-        DftP<R, false, R, NO>::run(a);
-      } else {
-        DftP<R, INV, NZ, R>::run(a);
-        twiddle();
-      }
-      sfor<NOUT>([&](auto jc) {
-        constexpr int j = decltype(jc)::value;
-        store(i, j, base + j * s, a[j]);
-      });
-    }
-  }
-}
-
-template <class PL, bool INV, int NZ, class GLoad>
-__device__ __forceinline__ void fft_dif(cplx *sbuf, int t, const cplx *__restrict__ tw,
-                                        const cplx *__restrict__ tw0, GLoad &&gload,
-                                        cplx (&out)[PL::V]) {
-  constexpr int RL = PL::Rlast;
-  constexpr int R0 = PL::radix[0];
-  auto g_load = [&](int, int, int pos) { return gload(pos); };
-  auto s_load = [&](int, int, int pos) { return sbuf[swz2(pos)]; };
-  auto s_store = [&](int, int, int pos, cplx v) { sbuf[swz2(pos)] = v; };
-  auto r_store = [&](int i, int j, int, cplx v) { out[i * RL + j] = v; };
-  static_assert(PL::P >= 2, "fast path needs at least two passes");
-  __syncthreads();
-  pass<PL, 0, INV, false, (NZ < R0 ? NZ : R0), R0>(t, tw, tw0, g_load, s_store);
-  sfor<PL::P - 2>([&](auto qc) {
-    constexpr int q = decltype(qc)::value + 1;
-    __syncthreads();
-    pass<PL, q, INV, false, PL::radix[q], PL::radix[q]>(t, tw, tw0, s_load, s_store);
-  });
-  __syncthreads();
-  pass<PL, PL::P - 1, INV, false, RL, RL>(t, tw, tw0, s_load, r_store);
-}
-
-template <class PL, int NO, class GStore>
-__device__ __forceinline__ void fft_final(cplx *sbuf, int t, const cplx *__restrict__ tw,
-                                          const cplx *__restrict__ tw0, cplx (&in)[PL::V],
-                                          GStore &&gstore) {
-  constexpr int RL = PL::Rlast;
-  constexpr int R0 = PL::radix[0];
-  auto r_load = [&](int i, int j, int) { return in[i * RL + j]; };
-  auto s_load = [&](int, int, int pos) { return sbuf[swz2(pos)]; };
-  auto s_store = [&](int, int, int pos, cplx v) { sbuf[swz2(pos)] = v; };
-  auto g_store = [&](int, int, int pos, cplx v) { gstore(pos, v); };
-  __syncthreads();
-  pass<PL, PL::P - 1, false, true, RL, RL>(t, tw, tw0, r_load, s_store);
-  sfor<PL::P - 2>([&](auto qc) {
-    constexpr int q = PL::P - 2 - decltype(qc)::value;
-    __syncthreads();
-    pass<PL, q, false, true, PL::radix[q], PL::radix[q]>(t, tw, tw0, s_load, s_store);
-  });
-  __syncthreads();
-  pass<PL, 0, false, true, R0, (NO < R0 ? NO : R0)>(t, tw, tw0, s_load, g_store);
-}
-
-__device__ __forceinline__ cplx load_elem(const Factor &f, long long off, int pos, double scale) {
-  if (pos >= f.len) return make_double2(0.0, 0.0);
-  const long long k = (long long)pos * f.estride;
-  if (f.kind == FK_F64) {
-    const double *p = static_cast<const double *>(f.ptr) + off;
-    return make_double2(__ldg(p + k) * scale, 0.0);
-  }
-  const cplx *p = static_cast<const cplx *>(f.ptr) + off;
-  cplx v = __ldg(p + k);
-  return make_double2(v.x * scale, v.y * scale);
-}
 
 // L2 prefetch (cp.async.bulk.prefetch.L2) of one operand item, if contiguous.
 __device__ __forceinline__ void prefetch_item(const Factor &f, long long b, long long nsub,
@@ -216,7 +75,7 @@ __global__ void __launch_bounds__(PL::CTA, Traits<PL>::min_blocks)
   const long long nblk = (a.batch + PL::G - 1) / PL::G;
   cplx *sbuf = smem + g * PL::L;
   const cplx *__restrict__ tw = a.tw;
-  const cplx *__restrict__ tw0 = a.tw0;
+  const Tw0Global tw0{a.tw0, PL::L / PL::radix[0], PL::radix[0]};
   const bool do_pf = a.prefetch != 0;
   if (do_pf && threadIdx.x == 0) prefetch_block(a, blockIdx.x, PL::G);
 

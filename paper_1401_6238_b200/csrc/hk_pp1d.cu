@@ -1,0 +1,278 @@
+// K1 producer/consumer variant for the batched H x^{m-1} workload (cfg2):
+// one 512-thread CTA per SM runs two product groups in ping-pong while the
+// Tensor Memory Accelerator streams the next operands into shared memory.
+//
+//   smem : ex[2][L] (per-group exchange) | hst[L] (h staging, shared by the
+//          two groups in turn) | xst[2][XS] (per-group x staging)
+//   TMEM : cols [0,256)   spectral accumulator (ifft(h) .* fft(x)^p), per thread
+//          cols [256,512) the thread's first-pass twiddles W_L^{j t}, j=1..R0-1,
+//          loaded once per CTA (they are identical for every product)
+//   sync : mbarrier complete_tx for TMA arrivals, named barrier per group
+//
+// Product k of a CTA belongs to group k&1.  Group g, after the first pass of
+// ifft(h_k) has consumed hst, hands hst to the TMA for h_{k+1} (the other
+// group's next product); after the first pass of fft(x_k) it refills its own
+// xst with x_{k+2}.  The copy engine therefore runs a full half-period ahead
+// of the math, global-load latency leaves the critical path, and the two
+// groups drift into the anti-phase that keeps the FP64 pipe busy while the
+// other group is in a barrier.
+//
+// Math per product is exactly the fast kernel's (hk_fastcore.cuh), so the
+// result is bit-identical to it.
+#include <atomic>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include "hk_fastcore.cuh"
+
+namespace hk {
+namespace pp {
+
+using fast::pass;
+using fast::swz2;
+
+__device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(addr), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t addr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(addr), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load(uint32_t dst, const void *src, uint32_t bytes,
+                                         uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+template <int ID, int N>
+struct NamedSync {
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;\n" ::"n"(ID), "n"(N) : "memory");
+  }
+};
+
+// First-pass twiddles from this thread's TMEM slab.
+struct Tw0Tmem {
+  uint32_t taddr;
+  __device__ __forceinline__ void chunk(int, int c, cplx *w) const { tmem_ld4(taddr + 16 * c, w); }
+};
+
+template <class PL>
+struct Layout {
+  static constexpr int L = PL::L;
+  static constexpr int T = PL::T;
+  static_assert(PL::G == 1 && T == 256, "ping-pong kernel: one product per 256-thread group");
+  static_assert(PL::L / PL::radix[0] == T, "first pass: one butterfly per thread");
+};
+
+template <class PL, int NZ, int NO>
+__global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constant__ Args1D a) {
+  constexpr int L = PL::L, T = PL::T, V = PL::V, R0 = PL::radix[0];
+  constexpr int S0 = PL::stride(0);
+  constexpr int XS = NZ * S0;  // staged x elements
+  (void)Layout<PL>{};
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t mbar[4];  // full_h[0..1], full_x[0..1]
+  __shared__ uint32_t tmem_slot;
+  cplx *ex = reinterpret_cast<cplx *>(smem_raw);
+  cplx *hst = ex + 2 * L;
+  cplx *xst = hst + L;
+
+  const int warp = threadIdx.x >> 5;
+  const int g = threadIdx.x / T;
+  const int t = threadIdx.x - g * T;
+  const uint32_t mb_h0 = smem_u32(&mbar[0]), mb_x0 = smem_u32(&mbar[2]);
+
+  if (warp == 0) tmem_alloc<512>(&tmem_slot);
+  if (threadIdx.x == 32) {
+    for (int i = 0; i < 4; ++i) mbar_init(smem_u32(&mbar[i]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t lane_q = (uint32_t)(32 * (warp & 3)) << 16;
+  const uint32_t tacc = tmem_slot + lane_q + (uint32_t)((warp >> 2) * 64);
+  const uint32_t ttw = tmem_slot + lane_q + 256u + (uint32_t)((warp >> 2) * 64);
+
+  // this thread's first-pass twiddles W_L^{j t} -> TMEM (same for every product)
+  {
+    const fast::Tw0Global g0{a.tw0, L / R0, R0};
+#pragma unroll
+    for (int c = 0; c < (R0 - 1 + 3) / 4; ++c) {
+      cplx w[4];
+      g0.chunk(t, c, w);
+      tmem_st4(ttw + 16 * c, w);
+    }
+    tmem_wait_st();
+  }
+  const Tw0Tmem tw0{ttw};
+
+  const long long B = a.batch;
+  const long long grid = gridDim.x;
+  const long long nloc = B > blockIdx.x ? (B - blockIdx.x + grid - 1) / grid : 0;
+  const Factor &hf = a.h;
+  const Factor &xf = a.fac[0];
+  const uint32_t hbytes = (uint32_t)hf.len * 16u;
+  const uint32_t xbytes = (uint32_t)xf.len * 16u;
+  auto hsrc = [&](long long k) {
+    return static_cast<const cplx *>(hf.ptr) + (blockIdx.x + k * grid) * hf.bstride;
+  };
+  auto xsrc = [&](long long k) {
+    return static_cast<const cplx *>(xf.ptr) + (blockIdx.x + k * grid) * xf.bstride;
+  };
+  if (threadIdx.x == 0) {
+    if (nloc > 0) {
+      mbar_expect_tx(mb_h0, hbytes);
+      tma_load(smem_u32(hst), hsrc(0), hbytes, mb_h0);
+      mbar_expect_tx(mb_x0, xbytes);
+      tma_load(smem_u32(xst), xsrc(0), xbytes, mb_x0);
+    }
+    if (nloc > 1) {
+      mbar_expect_tx(mb_x0 + 8, xbytes);
+      tma_load(smem_u32(xst + XS), xsrc(1), xbytes, mb_x0 + 8);
+    }
+  }
+
+  cplx *sbuf = ex + g * L;
+  cplx *my_x = xst + g * XS;
+  const cplx *__restrict__ tw = a.tw;
+  const double sc = a.scale;
+  const int hlen = hf.len, xlen = xf.len, power = xf.power;
+  const int n1 = a.out_len;
+
+  auto run = [&](auto sync) {
+    int kk = 0;
+    for (long long k = g; k < nloc; k += 2, ++kk) {
+      const uint32_t par = (uint32_t)(kk & 1);
+      const long long prod = blockIdx.x + k * grid;
+      cplx v[V];
+      // ---- S = ifft(h~) from staged h; release hst to the TMA for product k+1
+      mbar_wait(mb_h0 + 8 * g, par);
+      fast::fft_dif<PL, true, R0>(
+          sbuf, t, tw, tw0,
+          [&](int pos) {
+            if (pos >= hlen) return make_double2(0.0, 0.0);
+            const cplx h = hst[pos];
+            return make_double2(h.x * sc, h.y * sc);
+          },
+          v, sync, [&]() {
+            if (t == 0 && k + 1 < nloc) {
+              const uint32_t mb = mb_h0 + 8 * (1 - g);
+              fence_proxy_async();
+              mbar_expect_tx(mb, hbytes);
+              tma_load(smem_u32(hst), hsrc(k + 1), hbytes, mb);
+            }
+          });
+      tmem_wait_st();
+#pragma unroll
+      for (int c = 0; c < V / 4; ++c) tmem_st4(tacc + 16 * c, &v[4 * c]);
+      // ---- X = fft(x~) from staged x; refill this group's xst with product k+2
+      mbar_wait(mb_x0 + 8 * g, par);
+      fast::fft_dif<PL, false, NZ>(
+          sbuf, t, tw, tw0,
+          [&](int pos) { return pos < xlen ? my_x[pos] : make_double2(0.0, 0.0); }, v, sync,
+          [&]() {
+            if (t == 0 && k + 2 < nloc) {
+              const uint32_t mb = mb_x0 + 8 * g;
+              fence_proxy_async();
+              mbar_expect_tx(mb, xbytes);
+              tma_load(smem_u32(my_x), xsrc(k + 2), xbytes, mb);
+            }
+          });
+      tmem_wait_st();
+#pragma unroll
+      for (int c = 0; c < V / 4; ++c) {
+        cplx acc[4];
+        tmem_ld4(tacc + 16 * c, acc);
+        for (int q = 0; q < power; ++q) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[e] = cmul(acc[e], v[4 * c + e]);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[4 * c + e] = acc[e];
+      }
+      // ---- y = fft(acc)[:n_1]
+      cplx *y = static_cast<cplx *>(a.out) + prod * a.out_bstride;
+      fast::fft_final<PL, NO>(sbuf, t, tw, tw0, v, [&](int pos, cplx val) {
+        if (pos < n1) y[pos] = val;
+      }, sync);
+    }
+  };
+  if (g == 0)
+    run(NamedSync<1, T>());
+  else
+    run(NamedSync<2, T>());
+
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tmem_fence_after();
+    tmem_dealloc<512>(tmem_slot);
+  }
+}
+
+template <class PL, int NZ, int NO>
+static cudaError_t launch_pp(const Args1D &a, cudaStream_t stream) {
+  constexpr int XS = NZ * PL::stride(0);
+  const int smem = (3 * PL::L + 2 * XS) * (int)sizeof(cplx);
+  static std::atomic<unsigned long long> configured{0};
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(configured.load() & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(k_hankel_pp<PL, NZ, NO>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+    configured.fetch_or(bit);
+  }
+  long long grid = sms[dev & 63];
+  if (const char *e = getenv("HK_PP_GRID")) grid = atoi(e);
+  if (grid > a.batch) grid = a.batch;
+  if (grid <= 0) return cudaSuccess;
+  k_hankel_pp<PL, NZ, NO><<<(unsigned)grid, 2 * PL::T, smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace pp
+
+// Ping-pong TMA path; cudaErrorNotSupported unless the request is the plain
+// batched H x^{m-1} shape it implements.
+cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream) {
+  if (getenv("HK_NO_PP")) return cudaErrorNotSupported;
+  if (L != 4096 || a.mode != M_PARTIAL || a.nfac != 1 || !a.tw0 || a.nsub != 1)
+    return cudaErrorNotSupported;
+  const Factor &h = a.h, &x = a.fac[0];
+  if (h.kind != FK_C128 || x.kind != FK_C128 || h.estride != 1 || x.estride != 1 ||
+      a.out_estride != 1)
+    return cudaErrorNotSupported;
+  if ((reinterpret_cast<uintptr_t>(h.ptr) | reinterpret_cast<uintptr_t>(x.ptr)) & 15)
+    return cudaErrorNotSupported;
+  if (h.len > L || h.len <= 0 || x.len <= 0) return cudaErrorNotSupported;
+  using PL = Plan1D<4096, 256, 16, 16, 16>;
+  constexpr int s0 = PL::stride(0);
+  const int nz = (x.len + s0 - 1) / s0, no = (a.out_len + s0 - 1) / s0;
+  if (nz <= 4 && no <= 4) return pp::launch_pp<PL, 4, 4>(a, stream);
+  return cudaErrorNotSupported;  // x staging would not fit next to three L buffers
+}
+
+}  // namespace hk
