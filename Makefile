@@ -15,9 +15,14 @@ HDRS := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.h) include/hankelfft_b200.h
 
 all: $(LIB)
 
+# per-file ptxas options: the ping-pong kernel keeps 3 transforms' worth of
+# swizzled addresses live under -O3 scheduling and spills at 128 registers;
+# ptxas -O1 schedules it in 125 registers with no spills.
+PTXAS_hk_pp1d := -Xptxas -O1
+
 $(OBJ)/%.o: $(SRC)/%.cu $(HDRS) Makefile
 	@mkdir -p $(OBJ)
-	$(NVCC) $(NVFLAGS) -c $< -o $@
+	$(NVCC) $(NVFLAGS) $(PTXAS_$*) -c $< -o $@
 
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart_static -lrt -lpthread -ldl

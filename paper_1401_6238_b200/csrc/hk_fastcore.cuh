@@ -90,9 +90,20 @@ __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const T
             });
           });
         } else if constexpr (p < PL::P - 1) {
-          sfor<R>([&](auto jc) {
-            constexpr int j = decltype(jc)::value;
-            if constexpr (j > 0) a[j] = cmul_dir<INV>(a[j], __ldg(&tw[j * lo * (PL::L / Lp)]));
+          // chunks of 4 loads behind a compiler fence: the scheduler may not
+          // hoist all R-1 twiddles (4(R-1) registers) above the butterfly
+          sfor<(R - 1 + 3) / 4>([&](auto cc) {
+            constexpr int c = decltype(cc)::value;
+            asm volatile("" ::: "memory");
+            cplx w[4];
+            sfor<4>([&](auto qc) {
+              constexpr int j = 4 * c + decltype(qc)::value + 1;
+              if constexpr (j < R) w[decltype(qc)::value] = __ldg(&tw[j * lo * (PL::L / Lp)]);
+            });
+            sfor<4>([&](auto qc) {
+              constexpr int j = 4 * c + decltype(qc)::value + 1;
+              if constexpr (j < R) a[j] = cmul_dir<INV>(a[j], w[decltype(qc)::value]);
+            });
           });
         }
       };

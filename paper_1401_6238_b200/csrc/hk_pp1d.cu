@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
 
   const int warp = threadIdx.x >> 5;
   const int g = threadIdx.x / T;
-  const int t = threadIdx.x - g * T;
+  const int t_in = threadIdx.x - g * T;
   const uint32_t mb_h0 = smem_u32(&mbar[0]), mb_x0 = smem_u32(&mbar[2]);
 
   if (warp == 0) tmem_alloc<512>(&tmem_slot);
@@ -118,83 +118,96 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
 #pragma unroll
     for (int c = 0; c < (R0 - 1 + 3) / 4; ++c) {
       cplx w[4];
-      g0.chunk(t, c, w);
+      g0.chunk(t_in, c, w);
       tmem_st4(ttw + 16 * c, w);
     }
     tmem_wait_st();
   }
   const Tw0Tmem tw0{ttw};
 
-  const long long B = a.batch;
-  const long long grid = gridDim.x;
-  const long long nloc = B > blockIdx.x ? (B - blockIdx.x + grid - 1) / grid : 0;
-  const Factor &hf = a.h;
-  const Factor &xf = a.fac[0];
-  const uint32_t hbytes = (uint32_t)hf.len * 16u;
-  const uint32_t xbytes = (uint32_t)xf.len * 16u;
-  auto hsrc = [&](long long k) {
-    return static_cast<const cplx *>(hf.ptr) + (blockIdx.x + k * grid) * hf.bstride;
-  };
-  auto xsrc = [&](long long k) {
-    return static_cast<const cplx *>(xf.ptr) + (blockIdx.x + k * grid) * xf.bstride;
-  };
+  // Everything the loop needs is either a kernel parameter (read from the
+  // constant bank at the point of use), a compile-time function of the group
+  // index G, or the thread index: this keeps the 128-register budget for data.
+  const long long nloc = a.batch > blockIdx.x
+                             ? (a.batch - blockIdx.x + gridDim.x - 1) / gridDim.x
+                             : 0;
   if (threadIdx.x == 0) {
+    const uint32_t hbytes = (uint32_t)a.h.len * 16u, xbytes = (uint32_t)a.fac[0].len * 16u;
     if (nloc > 0) {
       mbar_expect_tx(mb_h0, hbytes);
-      tma_load(smem_u32(hst), hsrc(0), hbytes, mb_h0);
+      tma_load(smem_u32(hst), static_cast<const cplx *>(a.h.ptr) + blockIdx.x * a.h.bstride,
+               hbytes, mb_h0);
       mbar_expect_tx(mb_x0, xbytes);
-      tma_load(smem_u32(xst), xsrc(0), xbytes, mb_x0);
+      tma_load(smem_u32(xst),
+               static_cast<const cplx *>(a.fac[0].ptr) + blockIdx.x * a.fac[0].bstride, xbytes,
+               mb_x0);
     }
     if (nloc > 1) {
       mbar_expect_tx(mb_x0 + 8, xbytes);
-      tma_load(smem_u32(xst + XS), xsrc(1), xbytes, mb_x0 + 8);
+      tma_load(smem_u32(xst + XS),
+               static_cast<const cplx *>(a.fac[0].ptr) + (blockIdx.x + gridDim.x) * a.fac[0].bstride,
+               xbytes, mb_x0 + 8);
     }
   }
 
-  cplx *sbuf = ex + g * L;
-  cplx *my_x = xst + g * XS;
-  const cplx *__restrict__ tw = a.tw;
-  const double sc = a.scale;
-  const int hlen = hf.len, xlen = xf.len, power = xf.power;
-  const int n1 = a.out_len;
-
-  auto run = [&](auto sync) {
+  auto run = [&](auto gc) {
+    constexpr int G = decltype(gc)::value;
+    const NamedSync<1 + G, T> sync;
+    cplx *sbuf = ex + G * L;
+    cplx *my_x = xst + G * XS;
     int kk = 0;
-    for (long long k = g; k < nloc; k += 2, ++kk) {
+    for (long long k = G; k < nloc; k += 2, ++kk) {
       const uint32_t par = (uint32_t)(kk & 1);
-      const long long prod = blockIdx.x + k * grid;
+      // A fresh opaque copy of the thread index per transform keeps the
+      // compiler from hoisting / sharing the swizzled smem addresses of all
+      // three transforms (cheap to recompute, ruinous to keep live: spills).
+      auto fresh_t = [&]() {
+        int x = t_in;
+        asm volatile("" : "+r"(x));
+        return x;
+      };
       cplx v[V];
       // ---- S = ifft(h~) from staged h; release hst to the TMA for product k+1
-      mbar_wait(mb_h0 + 8 * g, par);
+      mbar_wait(mb_h0 + 8 * G, par);
+      int t = fresh_t();
       fast::fft_dif<PL, true, R0>(
-          sbuf, t, tw, tw0,
+          sbuf, t, a.tw, tw0,
           [&](int pos) {
-            if (pos >= hlen) return make_double2(0.0, 0.0);
+            if (pos >= a.h.len) return make_double2(0.0, 0.0);
             const cplx h = hst[pos];
-            return make_double2(h.x * sc, h.y * sc);
+            return make_double2(h.x * a.scale, h.y * a.scale);
           },
           v, sync, [&]() {
             if (t == 0 && k + 1 < nloc) {
-              const uint32_t mb = mb_h0 + 8 * (1 - g);
+              const uint32_t mb = mb_h0 + 8 * (1 - G);
+              const uint32_t bytes = (uint32_t)a.h.len * 16u;
               fence_proxy_async();
-              mbar_expect_tx(mb, hbytes);
-              tma_load(smem_u32(hst), hsrc(k + 1), hbytes, mb);
+              mbar_expect_tx(mb, bytes);
+              tma_load(smem_u32(hst),
+                       static_cast<const cplx *>(a.h.ptr) +
+                           (blockIdx.x + (k + 1) * gridDim.x) * a.h.bstride,
+                       bytes, mb);
             }
           });
       tmem_wait_st();
 #pragma unroll
       for (int c = 0; c < V / 4; ++c) tmem_st4(tacc + 16 * c, &v[4 * c]);
       // ---- X = fft(x~) from staged x; refill this group's xst with product k+2
-      mbar_wait(mb_x0 + 8 * g, par);
+      mbar_wait(mb_x0 + 8 * G, par);
+      t = fresh_t();
       fast::fft_dif<PL, false, NZ>(
-          sbuf, t, tw, tw0,
-          [&](int pos) { return pos < xlen ? my_x[pos] : make_double2(0.0, 0.0); }, v, sync,
-          [&]() {
+          sbuf, t, a.tw, tw0,
+          [&](int pos) { return pos < a.fac[0].len ? my_x[pos] : make_double2(0.0, 0.0); }, v,
+          sync, [&]() {
             if (t == 0 && k + 2 < nloc) {
-              const uint32_t mb = mb_x0 + 8 * g;
+              const uint32_t mb = mb_x0 + 8 * G;
+              const uint32_t bytes = (uint32_t)a.fac[0].len * 16u;
               fence_proxy_async();
-              mbar_expect_tx(mb, xbytes);
-              tma_load(smem_u32(my_x), xsrc(k + 2), xbytes, mb);
+              mbar_expect_tx(mb, bytes);
+              tma_load(smem_u32(my_x),
+                       static_cast<const cplx *>(a.fac[0].ptr) +
+                           (blockIdx.x + (k + 2) * gridDim.x) * a.fac[0].bstride,
+                       bytes, mb);
             }
           });
       tmem_wait_st();
@@ -202,7 +215,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
       for (int c = 0; c < V / 4; ++c) {
         cplx acc[4];
         tmem_ld4(tacc + 16 * c, acc);
-        for (int q = 0; q < power; ++q) {
+        for (int q = 0; q < a.fac[0].power; ++q) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) acc[e] = cmul(acc[e], v[4 * c + e]);
         }
@@ -210,16 +223,21 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
         for (int e = 0; e < 4; ++e) v[4 * c + e] = acc[e];
       }
       // ---- y = fft(acc)[:n_1]
-      cplx *y = static_cast<cplx *>(a.out) + prod * a.out_bstride;
-      fast::fft_final<PL, NO>(sbuf, t, tw, tw0, v, [&](int pos, cplx val) {
-        if (pos < n1) y[pos] = val;
-      }, sync);
+      t = fresh_t();
+      fast::fft_final<PL, NO>(
+          sbuf, t, a.tw, tw0, v,
+          [&](int pos, cplx val) {
+            if (pos < a.out_len)
+              static_cast<cplx *>(a.out)[(blockIdx.x + k * gridDim.x) * a.out_bstride + pos] =
+                  val;
+          },
+          sync);
     }
   };
   if (g == 0)
-    run(NamedSync<1, T>());
+    run(std::integral_constant<int, 0>{});
   else
-    run(NamedSync<2, T>());
+    run(std::integral_constant<int, 1>{});
 
   tmem_fence_before();
   __syncthreads();

@@ -42,12 +42,7 @@ __device__ __forceinline__ void tmem_fence_before() {
 __device__ __forceinline__ void tmem_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 }
-__device__ __forceinline__ void tmem_wait_st() {
-  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ void tmem_wait_ld() {
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n"); }
 
 // 4 complex doubles = 16 consecutive 32-bit columns of this thread's lane.
 __device__ __forceinline__ void tmem_st4(uint32_t taddr, const cplx *v) {
@@ -64,22 +59,22 @@ __device__ __forceinline__ void tmem_st4(uint32_t taddr, const cplx *v) {
       "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};\n" ::"r"(taddr),
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
       "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
-      "r"(r[15])
-      : "memory");
+      "r"(r[15]));
 }
 
-// Issue a load of 4 complex doubles; call tmem_wait_ld() before using v.
+// Load 4 complex doubles; the wait is inside the same asm block so the
+// outputs are valid when it returns (no memory clobber: TMEM is not generic
+// memory, and volatile asm keeps program order among TMEM operations).
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, cplx *v) {
   uint32_t r[16];
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
       "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];\n"
+      "tcgen05.wait::ld.sync.aligned;\n"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
         "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
         "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr)
-      : "memory");
-  tmem_wait_ld();
+      : "r"(taddr));
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     v[i].x = __hiloint2double((int)r[4 * i + 1], (int)r[4 * i + 0]);
