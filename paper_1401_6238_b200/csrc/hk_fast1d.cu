@@ -59,9 +59,9 @@ __global__ void __launch_bounds__(PL::CTA, Traits<PL>::min_blocks)
   constexpr int T = PL::T;
   constexpr int V = PL::V;
   constexpr int COLS = Tr::tmem_cols;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
-  cplx *smem = reinterpret_cast<cplx *>(smem_raw);
+  cplx *smem = reinterpret_cast<cplx *>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
   const int warp = threadIdx.x >> 5;
   if (warp == 0) tmem_alloc<COLS>(&tmem_slot);
   tmem_fence_before();
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(PL::CTA, Traits<PL>::min_blocks)
 
 template <class PL, int NZ, int NO>
 static cudaError_t launch_variant(const Args1D &a, cudaStream_t stream) {
-  const int smem = PL::G * PL::L * (int)sizeof(cplx);
+  const int smem = PL::G * PL::L * (int)sizeof(cplx) + 128;
   static std::atomic<unsigned long long> configured{0};
   int dev = 0;
   cudaGetDevice(&dev);

@@ -12,6 +12,70 @@ namespace fast {
 
 __device__ __forceinline__ int swz2(int pos) { return pos ^ (((pos >> 4) ^ (pos >> 8)) & 7); }
 
+// Cheap addressing of swz2-swizzled shared memory for radix-16 plans with
+// L <= 4096 (positions = 3 hex digits d2 d1 d0).  In the pass over hex digit q
+// a butterfly touches pos = base + j*16^q, and
+//   swz2(pos) = B + J(j) + (U ^ (j & 7))
+// with per-thread B, U and compile-time J(j): one base register plus at most
+// seven XOR-with-immediate ops cover all 16 accesses, which then use
+// immediate offsets (instead of ~5 integer ops per access).
+template <int Q>
+struct HexAddr {
+  uint32_t r0;  // shared-space byte address for j & 7 == 0, J == 0
+  __device__ __forceinline__ HexAddr(uint32_t sbase, int base) {
+    const int d0 = base & 15, d1 = (base >> 4) & 15, d2 = (base >> 8) & 15;
+    int B, U;
+    if constexpr (Q == 2) {
+      B = 16 * d1 + (d0 & 8);
+      U = (d0 ^ d1) & 7;
+    } else if constexpr (Q == 1) {
+      B = 256 * d2 + (d0 & 8);
+      U = (d0 ^ d2) & 7;
+    } else {
+      B = 256 * d2 + 16 * d1;
+      U = (d1 ^ d2) & 7;
+    }
+    r0 = sbase + 16u * (uint32_t)(B + U);
+  }
+  template <int J>
+  static constexpr int imm() {
+    return Q == 2 ? 16 * 256 * J : (Q == 1 ? 16 * 16 * J : 16 * (J & 8));
+  }
+  template <int J>
+  __device__ __forceinline__ uint32_t reg() const {
+    return r0 ^ (uint32_t)(16 * (J & 7));
+  }
+  template <int J>
+  __device__ __forceinline__ cplx ld() const {
+    cplx v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+%3];\n"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "r"(reg<J>()), "n"(imm<J>())
+                 : "memory");
+    return v;
+  }
+  template <int J>
+  __device__ __forceinline__ void st(cplx v) const {
+    asm volatile("st.shared.v2.f64 [%0+%1], {%2, %3};\n" ::"r"(reg<J>()), "n"(imm<J>()),
+                 "d"(v.x), "d"(v.y)
+                 : "memory");
+  }
+};
+
+template <class PL>
+constexpr bool hex_plan() {
+  if (PL::L > 4096) return false;
+  for (int q = 0; q < PL::P; ++q)
+    if (PL::radix[q] != 16) return false;
+  return true;
+}
+
+// Marker functors: a pass whose Load / Store is SmemIO uses HexAddr addressing
+// of the swizzled exchange buffer at `sbase` (shared-space byte address).
+struct SmemIO {
+  uint32_t sbase;
+};
+
 template <class PL>
 struct Traits {
   static constexpr int hi_count(int p) { return PL::L / (PL::stride(p) * PL::radix[p]); }
@@ -72,11 +136,20 @@ __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const T
         hi = beta / s;
       }
       const int base = hi * Lp + lo;
+      constexpr int Q = PL::P - 1 - p;
       cplx a[R];
-      sfor<NIN>([&](auto jc) {
-        constexpr int j = decltype(jc)::value;
-        a[j] = load(i, j, base + j * s);
-      });
+      if constexpr (std::is_same_v<std::decay_t<Load>, SmemIO>) {
+        const HexAddr<Q> ad(load.sbase, base);
+        sfor<NIN>([&](auto jc) {
+          constexpr int j = decltype(jc)::value;
+          a[j] = ad.template ld<j>();
+        });
+      } else {
+        sfor<NIN>([&](auto jc) {
+          constexpr int j = decltype(jc)::value;
+          a[j] = load(i, j, base + j * s);
+        });
+      }
       auto twiddle = [&]() {
         if constexpr (p == 0 && PL::P > 1) {
           // chunks of 4 twiddles (j = 4c+1 .. 4c+4) keep register pressure flat
@@ -114,16 +187,35 @@ __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const T
         DftP<R, INV, NZ, R>::run(a);
         twiddle();
       }
-      sfor<NOUT>([&](auto jc) {
-        constexpr int j = decltype(jc)::value;
-        store(i, j, base + j * s, a[j]);
-      });
+      if constexpr (std::is_same_v<std::decay_t<Store>, SmemIO>) {
+        const HexAddr<Q> ad(store.sbase, base);
+        sfor<NOUT>([&](auto jc) {
+          constexpr int j = decltype(jc)::value;
+          ad.template st<j>(a[j]);
+        });
+      } else {
+        sfor<NOUT>([&](auto jc) {
+          constexpr int j = decltype(jc)::value;
+          store(i, j, base + j * s, a[j]);
+        });
+      }
     }
   }
 }
 
+template <class PL, class Lambda>
+__device__ __forceinline__ decltype(auto) pick_io(Lambda &l, const SmemIO &sio) {
+  if constexpr (hex_plan<PL>())
+    return (sio);
+  else
+    return (l);
+}
+
+// bar.sync as volatile asm: keeps the volatile ld/st.shared of HexAddr ordered
 struct CtaSync {
-  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync 0;\n" ::: "memory");
+  }
 };
 
 struct NoHook {
@@ -140,9 +232,12 @@ __device__ __forceinline__ void fft_dif(cplx *sbuf, int t, const cplx *__restric
   constexpr int RL = PL::Rlast;
   constexpr int R0 = PL::radix[0];
   auto g_load = [&](int, int, int pos) { return gload(pos); };
-  auto s_load = [&](int, int, int pos) { return sbuf[swz2(pos)]; };
-  auto s_store = [&](int, int, int pos, cplx v) { sbuf[swz2(pos)] = v; };
+  auto s_load_l = [&](int, int, int pos) { return sbuf[swz2(pos)]; };
+  auto s_store_l = [&](int, int, int pos, cplx v) { sbuf[swz2(pos)] = v; };
   auto r_store = [&](int i, int j, int, cplx v) { out[i * RL + j] = v; };
+  const SmemIO sio{smem_u32(sbuf)};
+  auto &&s_load = pick_io<PL>(s_load_l, sio);
+  auto &&s_store = pick_io<PL>(s_store_l, sio);
   static_assert(PL::P >= 2, "fast path needs at least two passes");
   sync();
   pass<PL, 0, INV, false, (NZ < R0 ? NZ : R0), R0>(t, tw, tw0, g_load, s_store);
@@ -164,9 +259,12 @@ __device__ __forceinline__ void fft_final(cplx *sbuf, int t, const cplx *__restr
   constexpr int RL = PL::Rlast;
   constexpr int R0 = PL::radix[0];
   auto r_load = [&](int i, int j, int) { return in[i * RL + j]; };
-  auto s_load = [&](int, int, int pos) { return sbuf[swz2(pos)]; };
-  auto s_store = [&](int, int, int pos, cplx v) { sbuf[swz2(pos)] = v; };
+  auto s_load_l = [&](int, int, int pos) { return sbuf[swz2(pos)]; };
+  auto s_store_l = [&](int, int, int pos, cplx v) { sbuf[swz2(pos)] = v; };
   auto g_store = [&](int, int, int pos, cplx v) { gstore(pos, v); };
+  const SmemIO sio{smem_u32(sbuf)};
+  auto &&s_load = pick_io<PL>(s_load_l, sio);
+  auto &&s_store = pick_io<PL>(s_store_l, sio);
   sync();
   pass<PL, PL::P - 1, false, true, RL, RL>(t, tw, tw0, r_load, s_store);
   sfor<PL::P - 2>([&](auto qc) {

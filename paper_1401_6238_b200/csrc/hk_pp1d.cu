@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t mbar[4];  // full_h[0..1], full_x[0..1]
   __shared__ uint32_t tmem_slot;
-  cplx *ex = reinterpret_cast<cplx *>(smem_raw);
+  cplx *ex = reinterpret_cast<cplx *>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
   cplx *hst = ex + 2 * L;
   cplx *xst = hst + L;
 
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
 template <class PL, int NZ, int NO>
 static cudaError_t launch_pp(const Args1D &a, cudaStream_t stream) {
   constexpr int XS = NZ * PL::stride(0);
-  const int smem = (3 * PL::L + 2 * XS) * (int)sizeof(cplx);
+  const int smem = (3 * PL::L + 2 * XS) * (int)sizeof(cplx) + 128;
   static std::atomic<unsigned long long> configured{0};
   static int sms[64] = {0};
   int dev = 0;
