@@ -88,6 +88,41 @@ class HankelDeviceCache:
         return T[0].cpu().numpy()
 
 
+class BhhbDeviceCache:
+    """Device state of a BHHB tensor routed to the native 2D block kernels."""
+
+    def __init__(self, order, block_shape, outer_shape, H):
+        self.order = order
+        self.block_shape = tuple(block_shape)
+        self.outer_shape = tuple(outer_shape)
+        self.H = H
+        self._per_dev = {}
+
+    def _H(self):
+        dev = require_cuda()
+        dH = self._per_dev.get(dev)
+        if dH is None:
+            dH = torch.from_numpy(np.ascontiguousarray(self.H)).to(f"cuda:{dev}").unsqueeze(0)
+            self._per_dev[dev] = dH
+        return dev, dH
+
+    def tvp_partial(self, xs) -> np.ndarray:
+        dev, dH = self._H()
+        uniq, idx = _dedupe(xs)
+        up = _upload(uniq, dev)
+        y = batched.bhhb_tvp_partial(dH, [up[i] for i in idx], self.order, self.block_shape,
+                                     self.outer_shape)
+        return y[0].cpu().numpy()
+
+    def tvp_full(self, xs) -> complex:
+        dev, dH = self._H()
+        uniq, idx = _dedupe(xs)
+        up = _upload(uniq, dev)
+        a = batched.bhhb_tvp_full(dH, [up[i] for i in idx], self.order, self.block_shape,
+                                  self.outer_shape)
+        return complex(a[0].item())
+
+
 def generic_times_matrices(tensor, mats) -> np.ndarray:
     """Column-combination loop of hankel.py:189-194 over any tensor exposing
     ``mode_sizes`` and ``tvp_partial`` (block tensors)."""

@@ -52,6 +52,15 @@ def hankel_plan(shape, device: int, fft_len: int = 0) -> N.Plan:
     return N.hankel_plan(shape, device, fft_len)
 
 
+def _workspace(plan: N.Plan, batch: int, device) -> torch.Tensor:
+    """Caller-owned device workspace (two-level plans; empty for on-chip plans).
+
+    Freed by the caching allocator after the call: the stream-ordered reuse
+    rule keeps it valid for the kernels already queued on this stream."""
+    nbytes = int(N.load_library().hk_workspace_bytes(plan.handle, batch))
+    return torch.empty((max(nbytes, 16),), dtype=torch.uint8, device=device)
+
+
 def hankel_spectrum(h: torch.Tensor, shape, fft_len: int = 0) -> torch.Tensor:
     """Batched cached spectrum S = ifft(h~) (reference hankel.py:37-40, 126-128).
 
@@ -63,8 +72,9 @@ def hankel_spectrum(h: torch.Tensor, shape, fft_len: int = 0) -> torch.Tensor:
         plan = hankel_plan(shape, dev, fft_len)
         B = h.shape[0]
         spec = torch.empty((B, plan.spectrum_len), dtype=torch.complex128, device=h.device)
+        ws = _workspace(plan, B, h.device)
         N.check(N.load_library().hk_spectrum(plan.handle, _operand(h, "h"), B, spec.data_ptr(),
-                                             None, _stream(dev)), "hk_spectrum")
+                                             ws.data_ptr(), _stream(dev)), "hk_spectrum")
     return spec
 
 
@@ -95,9 +105,10 @@ def hankel_tvp_partial(h: torch.Tensor, xs, shape, *, spectrum: bool = False,
             out = torch.empty((B, shape[0]), dtype=torch.complex128, device=h.device)
         _require_cuda(out, "out")
         ops = _vector_operands(xs, [f"xs[{i}]" for i in range(len(xs))])
+        ws = _workspace(plan, B, h.device)
         N.check(N.load_library().hk_tvp_partial(
             plan.handle, _operand(h, "h", spectrum), ops, len(xs), B, out.data_ptr(),
-            out.stride(0), None, _stream(dev)), "hk_tvp_partial")
+            out.stride(0), ws.data_ptr(), _stream(dev)), "hk_tvp_partial")
     return out
 
 
@@ -115,9 +126,10 @@ def hankel_tvp_full(h: torch.Tensor, xs, shape, *, spectrum: bool = False,
         plan = hankel_plan(shape, dev, fft_len)
         alpha = torch.empty((B,), dtype=torch.complex128, device=h.device)
         ops = _vector_operands(xs, [f"xs[{i}]" for i in range(len(xs))])
+        ws = _workspace(plan, B, h.device)
         N.check(N.load_library().hk_tvp_full(
-            plan.handle, _operand(h, "h", spectrum), ops, len(xs), B, alpha.data_ptr(), None,
-            _stream(dev)), "hk_tvp_full")
+            plan.handle, _operand(h, "h", spectrum), ops, len(xs), B, alpha.data_ptr(),
+            ws.data_ptr(), _stream(dev)), "hk_tvp_full")
     return alpha
 
 
@@ -157,6 +169,79 @@ def times_matrices(h: torch.Tensor, shape, mats, *, spectrum: bool = False,
                                       T[0].numel() if B else 0, ws.data_ptr(), _stream(dev)),
                 "hk_times_matrices")
     return T
+
+
+def _block_operand(t: torch.Tensor, name: str, length: int, spectrum: bool = False):
+    """(B, length) vectors or (B, rows, cols) generators flattened per item."""
+    _require_cuda(t, name)
+    flat = t.reshape(t.shape[0], -1)
+    if flat.shape[1] != length:
+        raise ValueError(f"{name} must have {length} entries per item")
+    return _operand(flat, name, spectrum), flat
+
+
+def bhhb_plan(order, block_shape, outer_shape, device: int, fft_lens=None) -> N.Plan:
+    return N.block_plan(order, (tuple(block_shape), tuple(outer_shape)), device, fft_lens)
+
+
+def bhhb_tvp_partial(H: torch.Tensor, xs, order, block_shape, outer_shape, *,
+                     spectrum: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Batched BHHB product y_b = vec(fft2(ifft2(H_b) .* prod fft2(X~_bp))[:n_1, :N_1])
+    (reference block.py:136-144).
+
+    H: (B, d_in, d_out) generating matrices (rows = inner index sums);
+    xs[p]: (B, n_{p+1} * N_{p+1}) column-stacked (F-order) vectors.
+    Returns (B, n_1 * N_1) complex128 column-stacked outputs.
+    """
+    block_shape, outer_shape = tuple(block_shape), tuple(outer_shape)
+    xs = list(xs)
+    if len(xs) != order - 1:
+        raise ValueError(f"expected {order - 1} vectors, got {len(xs)}")
+    dev = _dev_index(H)
+    B = H.shape[0]
+    with torch.cuda.device(dev):
+        plan = bhhb_plan(order, block_shape, outer_shape, dev)
+        hop, _ = _block_operand(H, "H", plan.spectrum_len if spectrum else
+                                (sum(block_shape) - order + 1) * (sum(outer_shape) - order + 1),
+                                spectrum)
+        ops = (N.Operand * len(xs))()
+        keep = []
+        for i, x in enumerate(xs):
+            ops[i], f = _block_operand(x, f"xs[{i}]", block_shape[i + 1] * outer_shape[i + 1])
+            keep.append(f)
+        n1 = block_shape[0] * outer_shape[0]
+        if out is None:
+            out = torch.empty((B, n1), dtype=torch.complex128, device=H.device)
+        ws = _workspace(plan, B, H.device)
+        N.check(N.load_library().hk_tvp_partial(plan.handle, hop, ops, len(xs), B,
+                                                out.data_ptr(), out.stride(0), ws.data_ptr(),
+                                                _stream(dev)), "hk_tvp_partial(block)")
+    return out
+
+
+def bhhb_tvp_full(H: torch.Tensor, xs, order, block_shape, outer_shape) -> torch.Tensor:
+    """alpha_b = sum(ifft2(H_b) .* prod fft2(X~_bp)), unconjugated (block.py:146-153)."""
+    block_shape, outer_shape = tuple(block_shape), tuple(outer_shape)
+    xs = list(xs)
+    if len(xs) != order:
+        raise ValueError(f"expected {order} vectors, got {len(xs)}")
+    dev = _dev_index(H)
+    B = H.shape[0]
+    with torch.cuda.device(dev):
+        plan = bhhb_plan(order, block_shape, outer_shape, dev)
+        hop, _ = _block_operand(
+            H, "H", (sum(block_shape) - order + 1) * (sum(outer_shape) - order + 1))
+        ops = (N.Operand * len(xs))()
+        keep = []
+        for i, x in enumerate(xs):
+            ops[i], f = _block_operand(x, f"xs[{i}]", block_shape[i] * outer_shape[i])
+            keep.append(f)
+        alpha = torch.empty((B,), dtype=torch.complex128, device=H.device)
+        ws = _workspace(plan, B, H.device)
+        N.check(N.load_library().hk_tvp_full(plan.handle, hop, ops, len(xs), B,
+                                             alpha.data_ptr(), ws.data_ptr(), _stream(dev)),
+                "hk_tvp_full(block)")
+    return alpha
 
 
 class _HostPipeline:

@@ -3,7 +3,9 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <stdarg.h>
 #include <stdio.h>
@@ -13,6 +15,7 @@
 
 #include "../../include/hankelfft_b200.h"
 #include "hk_internal.h"
+#include "hk_large.h"
 
 using hk::Args1D;
 using hk::Factor;
@@ -28,6 +31,15 @@ struct hk_plan {
   std::vector<int64_t> L;       // per level FFT length
   const double2 *tw = nullptr;  // 1D twiddle table (length L[0])
   const double2 *tw0 = nullptr; // thread-major first-pass table for the fast kernels
+  // two-level plans (large 1D four-step or 2D block): L1 columns x L2 rows
+  int two_level = 0;
+  int twiddle = 0;               // 1D four-step (1) or 2D block (0)
+  long long L1 = 0, L2 = 0;
+  const double2 *thi = nullptr, *tlo = nullptr;    // four-step twiddles
+  const double2 *ctw = nullptr, *ctw0 = nullptr;   // column plan tables (L1)
+  const double2 *rtw = nullptr, *rtw0 = nullptr;   // row plan tables (L2)
+  // block plans: inner (block) and outer sizes per mode
+  std::vector<int64_t> inner, outer;
 };
 
 namespace {
@@ -91,7 +103,7 @@ std::map<std::pair<int, long long>, double2 *> g_tw0;
 
 int get_twiddles0(int device, long long L, int R0, const double2 **out) {
   std::lock_guard<std::mutex> lk(g_tw_mu);
-  auto key = std::make_pair(device, L);
+  auto key = std::make_pair(device, L * 1024 + R0);
   auto it = g_tw0.find(key);
   if (it != g_tw0.end()) {
     *out = it->second;
@@ -124,6 +136,83 @@ int get_twiddles0(int device, long long L, int R0, const double2 **out) {
   g_tw0[key] = d;
   *out = d;
   return HK_OK;
+}
+
+// W_L^{q*step}, q < count (four-step twiddle tables), per (device, L, step).
+std::map<std::tuple<int, long long, long long>, double2 *> g_tws;
+
+int get_twiddles_step(int device, long long L, long long step, long long count,
+                      const double2 **out) {
+  std::lock_guard<std::mutex> lk(g_tw_mu);
+  auto key = std::make_tuple(device, L, step);
+  auto it = g_tws.find(key);
+  if (it != g_tws.end()) {
+    *out = it->second;
+    return HK_OK;
+  }
+  std::vector<double2> host(count);
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  for (long long q = 0; q < count; ++q) {
+    const long long e = (q * step) % L;
+    long double ang = two_pi * (long double)e / (long double)L;
+    host[q].x = (double)cosl(ang);
+    host[q].y = (double)-sinl(ang);
+    if (e == 0) host[q] = make_double2(1.0, 0.0);
+    if (4 * e == L) host[q] = make_double2(0.0, -1.0);
+    if (2 * e == L) host[q] = make_double2(-1.0, 0.0);
+    if (4 * e == 3 * L) host[q] = make_double2(0.0, 1.0);
+  }
+  double2 *d = nullptr;
+  cudaError_t err = cudaMalloc(&d, count * sizeof(double2));
+  if (err != cudaSuccess) return cuda_fail(err, "cudaMalloc(twiddles)");
+  err = cudaMemcpy(d, host.data(), count * sizeof(double2), cudaMemcpyHostToDevice);
+  if (err != cudaSuccess) {
+    cudaFree(d);
+    return cuda_fail(err, "cudaMemcpy(twiddles)");
+  }
+  g_tws[key] = d;
+  *out = d;
+  return HK_OK;
+}
+
+// Tables of a length used as a row (fast / generic 1D kernel) or a column plan.
+int line_tables(int dev, long long L, const double2 **tw, const double2 **tw0) {
+  int rc = get_twiddles(dev, L, tw);
+  if (rc) return rc;
+  const int r0 = hk::fast_first_radix(L);
+  *tw0 = nullptr;
+  if (r0 > 0) rc = get_twiddles0(dev, L, r0, tw0);
+  return rc;
+}
+
+int col_tables(int dev, long long L1, const double2 **tw, const double2 **tw0) {
+  // column plans: first radix of Plan1D<L1, ...> used in hk_large.cu
+  int r0 = 0;
+  switch (L1) {
+    case 8: r0 = 8; break;
+    case 12: r0 = 12; break;
+    case 16: r0 = 16; break;
+    case 24: r0 = 24; break;
+    case 32: r0 = 2; break;
+    case 48: r0 = 3; break;
+    case 64: r0 = 4; break;
+    case 96: r0 = 6; break;
+    case 128: r0 = 8; break;
+    case 192: r0 = 12; break;
+    case 256: r0 = 16; break;
+    case 384: r0 = 24; break;
+    case 512: r0 = 2; break;
+    case 768: r0 = 3; break;
+    case 1024: r0 = 4; break;
+    case 1536: r0 = 6; break;
+    case 2048: r0 = 8; break;
+    default: return fail(HK_EUNSUPPORTED, "no column plan of length %lld", L1);
+  }
+  int rc = get_twiddles(dev, L1, tw);
+  if (rc) return rc;
+  *tw0 = nullptr;
+  if (L1 <= 24) return HK_OK;  // single-pass column plans use no first-pass table
+  return get_twiddles0(dev, L1, r0, tw0);
 }
 
 int check_plan(const hk_plan *p) {
@@ -236,14 +325,12 @@ int hk_plan_create_hankel(hk_plan **plan, int order, const int64_t *mode_sizes, 
     d += mode_sizes[i];
   }
   d = d - order + 1;
-  long long L = fft_len > 0 ? fft_len : hk::choose_len_1d(d);
-  if (L < 0)
-    return fail(HK_EUNSUPPORTED, "d_H = %lld exceeds the largest on-chip FFT length", d);
-  if (L < d) return fail(HK_EINVAL, "fft_len %lld is shorter than d_H = %lld", L, d);
-  if (!hk::supported_1d(L)) return fail(HK_EUNSUPPORTED, "FFT length %lld is not supported", L);
+  if (fft_len > 0 && fft_len < d)
+    return fail(HK_EINVAL, "fft_len %lld is shorter than d_H = %lld", (long long)fft_len, d);
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  long long L = fft_len > 0 ? fft_len : hk::choose_len_1d(d);
   hk_plan *p = new hk_plan();
   p->kind = 1;
   p->order = order;
@@ -251,10 +338,45 @@ int hk_plan_create_hankel(hk_plan **plan, int order, const int64_t *mode_sizes, 
   p->device = dev;
   p->sizes.assign(mode_sizes, mode_sizes + order);
   p->dof = {d};
-  p->L = {L};
-  int rc = get_twiddles(dev, L, &p->tw);
-  const int r0 = hk::fast_first_radix(L);
-  if (!rc && r0 > 0) rc = get_twiddles0(dev, L, r0, &p->tw0);
+  int rc = HK_OK;
+  if (L > 0 && hk::supported_1d(L)) {
+    p->L = {L};
+    rc = line_tables(dev, L, &p->tw, &p->tw0);
+  } else {
+    // two-level four-step: L = L1 * L2 (L1 column plan, L2 fast row plan)
+    long long best1 = 0, best2 = 0;
+    for (long long l2 : {256LL, 384LL, 512LL, 768LL, 1024LL, 1536LL, 2048LL, 3072LL, 4096LL,
+                         6144LL, 8192LL})
+      for (long long l1 : {8LL, 12LL, 16LL, 24LL, 32LL, 48LL, 64LL, 96LL, 128LL, 192LL, 256LL,
+                           384LL, 512LL, 768LL, 1024LL, 1536LL, 2048LL}) {
+        const long long l = l1 * l2;
+        if (fft_len > 0 ? l != fft_len : l < d) continue;
+        // smallest L; on ties prefer rows with a fast kernel, then fewer columns
+        const bool fast2 = hk::fast_first_radix(l2) > 0;
+        const bool bfast = best1 && hk::fast_first_radix(best2) > 0;
+        if (!best1 || l < best1 * best2 ||
+            (l == best1 * best2 && (fast2 > bfast || (fast2 == bfast && l1 < best1)))) {
+          best1 = l1;
+          best2 = l2;
+        }
+      }
+    if (!best1) {
+      delete p;
+      return fail(HK_EUNSUPPORTED, fft_len > 0 ? "FFT length %lld is not supported"
+                                               : "d_H = %lld exceeds the supported lengths",
+                  fft_len > 0 ? (long long)fft_len : d);
+    }
+    p->two_level = 1;
+    p->twiddle = 1;
+    p->L1 = best1;
+    p->L2 = best2;
+    p->L = {best1 * best2};
+    const long long Lt = best1 * best2;
+    rc = line_tables(dev, best2, &p->rtw, &p->rtw0);
+    if (!rc) rc = col_tables(dev, best1, &p->ctw, &p->ctw0);
+    if (!rc) rc = get_twiddles_step(dev, Lt, 4096, (Lt + 4095) / 4096, &p->thi);
+    if (!rc) rc = get_twiddles_step(dev, Lt, 1, 4096, &p->tlo);
+  }
   if (rc) {
     delete p;
     return rc;
@@ -265,12 +387,65 @@ int hk_plan_create_hankel(hk_plan **plan, int order, const int64_t *mode_sizes, 
 
 int hk_plan_create_block(hk_plan **plan, int order, int levels, const int64_t *level_shapes,
                          const int64_t *fft_lens) {
-  (void)order;
-  (void)levels;
-  (void)level_shapes;
-  (void)fft_lens;
-  if (plan) *plan = nullptr;
-  return fail(HK_EUNSUPPORTED, "block plans are not built yet");
+  if (!plan) return fail(HK_EINVAL, "plan output pointer is NULL");
+  *plan = nullptr;
+  if (order < 2) return fail(HK_EINVAL, "order must be at least 2");
+  if (!level_shapes) return fail(HK_EINVAL, "level_shapes is NULL");
+  if (levels != 2)
+    return fail(HK_EUNSUPPORTED, "block plans cover 2 levels (BHHB); use the Kronecker 1D form");
+  long long din = 0, dout = 0;
+  std::vector<int64_t> inner(order), outer(order), sizes(order);
+  for (int i = 0; i < order; ++i) {
+    inner[i] = level_shapes[i];
+    outer[i] = level_shapes[order + i];
+    if (inner[i] < 1 || outer[i] < 1) return fail(HK_EINVAL, "shape entries must be positive");
+    din += inner[i];
+    dout += outer[i];
+    sizes[i] = inner[i] * outer[i];
+  }
+  din = din - order + 1;
+  dout = dout - order + 1;
+  long long L2 = fft_lens && fft_lens[0] > 0 ? fft_lens[0] : hk::choose_len_1d(din);
+  long long L1 = 0;
+  if (fft_lens && fft_lens[1] > 0) {
+    L1 = fft_lens[1];
+  } else {
+    for (long long l1 : {8LL, 12LL, 16LL, 24LL, 32LL, 48LL, 64LL, 96LL, 128LL, 192LL, 256LL,
+                         384LL, 512LL, 768LL, 1024LL, 1536LL, 2048LL})
+      if (l1 >= dout) {
+        L1 = l1;
+        break;
+      }
+  }
+  if (L2 < din || L1 < dout) return fail(HK_EINVAL, "fft lengths shorter than the generator");
+  if (L2 <= 0 || !hk::supported_1d(L2) || !hk::supported_col_len(L1))
+    return fail(HK_EUNSUPPORTED, "block generator %lldx%lld exceeds the supported lengths", din,
+                dout);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  hk_plan *p = new hk_plan();
+  p->kind = 2;
+  p->order = order;
+  p->levels = 2;
+  p->device = dev;
+  p->sizes = sizes;
+  p->inner = inner;
+  p->outer = outer;
+  p->dof = {din, dout};
+  p->L = {L2, L1};
+  p->two_level = 1;
+  p->twiddle = 0;
+  p->L1 = L1;
+  p->L2 = L2;
+  int rc = line_tables(dev, L2, &p->rtw, &p->rtw0);
+  if (!rc) rc = col_tables(dev, L1, &p->ctw, &p->ctw0);
+  if (rc) {
+    delete p;
+    return rc;
+  }
+  *plan = p;
+  return HK_OK;
 }
 
 int hk_plan_destroy(hk_plan *plan) {
@@ -290,10 +465,241 @@ int64_t hk_plan_spectrum_len(const hk_plan *plan) {
   return n;
 }
 
+namespace {
+// Items processed per two-level chunk (bounds the workspace to ~1 GiB).
+long long tl_per_item(const hk_plan *p) {
+  return (long long)(p->order + 2) * p->L1 * p->L2 + p->L1;  // Wh, order x Wx, Wq, row sums
+}
+long long tl_chunk(const hk_plan *p, long long batch) {
+  const long long cap = std::max(1LL, (1LL << 26) / tl_per_item(p));  // 2^26 complex = 1 GiB
+  return std::max(1LL, std::min(batch, cap));
+}
+}  // namespace
+
+
+namespace {
+
+int launch_row(long long L2, const Args1D &a, cudaStream_t st) {
+  cudaError_t e = cudaErrorNotSupported;
+  if (!g_force_generic) e = hk::launch_fast_1d((int)L2, a, st);
+  if (e == cudaErrorNotSupported) e = hk::launch_1d((int)L2, a, st);
+  if (e != cudaSuccess) return cuda_fail(e, "row-stage kernel launch");
+  return HK_OK;
+}
+
+int elem_bytes(int32_t dtype) { return dtype == HK_F64 ? 8 : 16; }
+
+// Operand of mode `mode` (0-based) of a two-level plan as an L1 x L2 array.
+hk::large::Op2 tl_vector_op(const hk_plan *p, const hk_operand &o, int mode, long long b0,
+                            int *ncols) {
+  hk::large::Op2 op{};
+  op.ptr = static_cast<const char *>(o.data) + b0 * o.batch_stride * elem_bytes(o.dtype);
+  op.item_stride = o.batch_stride;
+  op.kind = o.dtype == HK_F64 ? hk::FK_F64 : hk::FK_C128;
+  op.scale = 1.0;
+  if (p->twiddle) {  // 1D four-step
+    const long long n = p->sizes[mode];
+    op.s1 = p->L2;
+    op.s2 = 1;
+    op.len = n;
+    *ncols = (int)std::min<long long>(p->L2, n);
+  } else {  // 2D block: F-order (inner n x outer N), element (i, j) at i + n j
+    const long long n = p->inner[mode], N = p->outer[mode];
+    op.s1 = n;
+    op.s2 = 1;
+    op.len = -1;
+    op.e1 = (int32_t)N;
+    op.e2 = (int32_t)n;
+    *ncols = (int)n;
+  }
+  return op;
+}
+
+// what: 0 partial (y), 1 full (alpha), 2 spectrum (stage-A output of h)
+int tl_run(const hk_plan *p, const hk_operand &h, const hk_operand *xs, int nx, int mode_offset,
+           int64_t batch, void *out, int64_t out_stride, void *ws, void *stream, int what) {
+  if (batch == 0) return HK_OK;
+  if (!ws) return fail(HK_EINVAL, "two-level plans need a workspace of hk_workspace_bytes()");
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long L1 = p->L1, L2 = p->L2, L = L1 * L2;
+  // distinct vector factors
+  struct Fac {
+    hk_operand op;
+    int mode;
+    int power;
+  };
+  std::vector<Fac> fs;
+  for (int i = 0; i < nx; ++i) {
+    if (!xs[i].data) return fail(HK_EINVAL, "vector %d pointer is NULL", i);
+    if (xs[i].dtype != HK_C128 && xs[i].dtype != HK_F64)
+      return fail(HK_EINVAL, "vector %d: two-level plans take raw vectors", i);
+    const int mode = i + mode_offset;
+    bool merged = false;
+    for (auto &f : fs)
+      if (f.op.data == xs[i].data && f.op.batch_stride == xs[i].batch_stride &&
+          f.op.dtype == xs[i].dtype && p->sizes[f.mode] == p->sizes[mode] &&
+          (p->twiddle || (p->inner[f.mode] == p->inner[mode]))) {
+        ++f.power;
+        merged = true;
+        break;
+      }
+    if (!merged) fs.push_back({xs[i], mode, 1});
+  }
+  if ((int)fs.size() > p->order || (int)fs.size() > hk::kMaxFactors)
+    return fail(HK_EUNSUPPORTED, "too many distinct vectors for the two-level workspace");
+  const long long chunk = tl_chunk(p, batch);
+  double2 *W = static_cast<double2 *>(ws);
+  double2 *Wh = W;
+  double2 *Wx = Wh + chunk * L;
+  double2 *Wq = Wx + (long long)p->order * chunk * L;
+  double2 *part = Wq + chunk * L;
+
+  hk::large::ColArgs ca{};
+  ca.L1 = (int32_t)L1;
+  ca.L2 = (int32_t)L2;
+  ca.L = L;
+  ca.twiddle = p->twiddle;
+  ca.thi = p->thi;
+  ca.tlo = p->tlo;
+  ca.ctw = p->ctw;
+  ca.ctw0 = p->ctw0;
+  const long long d = p->dof[0];
+  const long long din = p->twiddle ? d : p->dof[0], dout = p->twiddle ? 0 : p->dof[1];
+  const int hcols = (int)(p->twiddle ? std::min(L2, d) : din);
+  int ocols = 0;
+  hk::large::Out2 yout{};
+  if (p->twiddle) {
+    ocols = (int)std::min<long long>(L2, p->sizes[0]);
+  } else {
+    ocols = (int)p->inner[0];
+  }
+  for (long long b0 = 0; b0 < batch; b0 += chunk) {
+    const long long nb = std::min(chunk, batch - b0);
+    cudaError_t e;
+    // ---- stage A: h (inverse, 1/L applied here)
+    const double2 *whp = Wh;
+    long long wh_item = L;
+    if (h.dtype == HK_SPEC) {
+      whp = static_cast<const double2 *>(h.data) + b0 * h.batch_stride;
+      wh_item = h.batch_stride;
+    } else {
+      ca.in = hk::large::Op2{};
+      ca.in.ptr = static_cast<const char *>(h.data) + b0 * h.batch_stride * elem_bytes(h.dtype);
+      ca.in.item_stride = h.batch_stride;
+      ca.in.kind = h.dtype == HK_F64 ? hk::FK_F64 : hk::FK_C128;
+      ca.in.scale = 1.0 / (double)L;
+      if (p->twiddle) {
+        ca.in.s1 = L2;
+        ca.in.s2 = 1;
+        ca.in.len = d;
+        ca.in_n1_fast = 0;
+      } else {  // H[s][t], s = inner sum (n2), t = outer sum (n1), t contiguous
+        ca.in.s1 = 1;
+        ca.in.s2 = dout;
+        ca.in.len = -1;
+        ca.in.e1 = (int32_t)dout;
+        ca.in.e2 = (int32_t)din;
+        ca.in_n1_fast = 1;
+      }
+      double2 *dst = what == 2 ? static_cast<double2 *>(out) + b0 * L : Wh;
+      ca.out = hk::large::Out2{dst, L, L2, 1, -1, (int32_t)L1, (int32_t)L2};
+      if ((e = hk::launch_cols(hk::large::ST_A_INV, ca, nb, hcols, st)) != cudaSuccess)
+        return cuda_fail(e, "column stage (h)");
+      if (what == 2) continue;
+    }
+    // ---- stage A: distinct vectors (forward)
+    Args1D a{};
+    a.batch = nb * L1;
+    a.nsub = L1;
+    a.tw = p->rtw;
+    a.tw0 = p->rtw0;
+    a.scale = 1.0;
+    a.prefetch = 1;
+    a.h.ptr = whp;
+    a.h.bstride = wh_item;
+    a.h.sstride = L2;
+    a.h.len = hcols;
+    a.h.power = 1;
+    a.h.kind = hk::FK_C128;
+    a.h.estride = 1;
+    a.nfac = (int)fs.size();
+    for (size_t f = 0; f < fs.size(); ++f) {
+      int ncols = 0;
+      ca.in = tl_vector_op(p, fs[f].op, fs[f].mode, b0, &ncols);
+      ca.in_n1_fast = 0;
+      double2 *wx = Wx + (long long)f * chunk * L;
+      ca.out = hk::large::Out2{wx, L, L2, 1, -1, (int32_t)L1, (int32_t)ncols};
+      if ((e = hk::launch_cols(hk::large::ST_A_FWD, ca, nb, ncols, st)) != cudaSuccess)
+        return cuda_fail(e, "column stage (x)");
+      hk::Factor &fa = a.fac[f];
+      fa.ptr = wx;
+      fa.bstride = L;
+      fa.sstride = L2;
+      fa.len = ncols;
+      fa.power = fs[f].power;
+      fa.kind = hk::FK_C128;
+      fa.estride = 1;
+    }
+    // ---- stage B: row products
+    if (what == 0) {
+      a.mode = hk::M_PARTIAL;
+      a.out = Wq;
+      a.out_bstride = L;
+      a.out_sstride = L2;
+      a.out_estride = 1;
+      a.out_len = ocols;
+    } else {
+      a.mode = hk::M_FULL;
+      a.out = part;
+      a.out_bstride = L1;
+      a.out_sstride = 1;
+      a.out_estride = 1;
+    }
+    int rc = launch_row(L2, a, st);
+    if (rc) return rc;
+    // ---- stage C: final column transform / reduction
+    if (what == 0) {
+      ca.in = hk::large::Op2{};
+      ca.in.ptr = Wq;
+      ca.in.item_stride = L;
+      ca.in.s1 = L2;
+      ca.in.s2 = 1;
+      ca.in.len = -1;
+      ca.in.e1 = (int32_t)L1;
+      ca.in.e2 = ocols;
+      ca.in.kind = hk::FK_C128;
+      ca.in.scale = 1.0;
+      ca.in_n1_fast = 0;
+      yout.ptr = static_cast<double2 *>(out) + b0 * out_stride;
+      yout.item_stride = out_stride;
+      if (p->twiddle) {
+        yout.s1 = L2;
+        yout.s2 = 1;
+        yout.len = p->sizes[0];
+      } else {
+        yout.s1 = p->inner[0];
+        yout.s2 = 1;
+        yout.len = -1;
+        yout.e1 = (int32_t)p->outer[0];
+        yout.e2 = (int32_t)p->inner[0];
+      }
+      ca.out = yout;
+      if ((e = hk::launch_cols(hk::large::ST_C, ca, nb, ocols, st)) != cudaSuccess)
+        return cuda_fail(e, "column stage (y)");
+    } else {
+      if ((e = hk::launch_rowsum(part, L1, static_cast<double2 *>(out) + b0, nb, st)) !=
+          cudaSuccess)
+        return cuda_fail(e, "row-sum kernel");
+    }
+  }
+  return HK_OK;
+}
+
+}  // namespace
+
 size_t hk_workspace_bytes(const hk_plan *plan, int64_t batch) {
-  (void)plan;
-  (void)batch;
-  return 0;
+  if (!plan || !plan->two_level || batch <= 0) return 0;
+  return (size_t)tl_chunk(plan, batch) * (size_t)tl_per_item(plan) * sizeof(double2);
 }
 
 int hk_spectrum(const hk_plan *plan, hk_operand h, int64_t batch, void *spec, void *workspace,
@@ -305,6 +711,7 @@ int hk_spectrum(const hk_plan *plan, hk_operand h, int64_t batch, void *spec, vo
   if (batch == 0) return HK_OK;
   if (h.dtype == HK_SPEC) return fail(HK_EINVAL, "h is already a spectrum");
   if (!spec) return fail(HK_EINVAL, "spec is NULL");
+  if (plan->two_level) return tl_run(plan, h, nullptr, 0, 0, batch, spec, 0, workspace, stream, 2);
   Args1D a = base_args(plan, batch);
   if ((rc = set_h(plan, h, a))) return rc;
   a.nfac = 0;
@@ -324,6 +731,7 @@ int hk_tvp_partial(const hk_plan *plan, hk_operand h, const hk_operand *xs, int 
   if (batch < 0) return fail(HK_EINVAL, "negative batch");
   if (batch == 0) return HK_OK;
   if (!y) return fail(HK_EINVAL, "y is NULL");
+  if (plan->two_level) return tl_run(plan, h, xs, nx, 1, batch, y, y_stride, workspace, stream, 0);
   Args1D a = base_args(plan, batch);
   if ((rc = set_h(plan, h, a))) return rc;
   if ((rc = set_vectors(plan, xs, nx, 1, a))) return rc;
@@ -343,6 +751,7 @@ int hk_tvp_full(const hk_plan *plan, hk_operand h, const hk_operand *xs, int nx,
   if (batch < 0) return fail(HK_EINVAL, "negative batch");
   if (batch == 0) return HK_OK;
   if (!alpha) return fail(HK_EINVAL, "alpha is NULL");
+  if (plan->two_level) return tl_run(plan, h, xs, nx, 0, batch, alpha, 1, workspace, stream, 1);
   Args1D a = base_args(plan, batch);
   if ((rc = set_h(plan, h, a))) return rc;
   if ((rc = set_vectors(plan, xs, nx, 0, a))) return rc;

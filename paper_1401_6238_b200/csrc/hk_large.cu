@@ -1,0 +1,220 @@
+// K3 / K4: two-level fused products for transforms that do not fit on chip.
+//
+// The length-L transform is viewed as an L1 x L2 array, element (n1, n2),
+// n2 contiguous.  Two modes share every kernel:
+//   * 1D (four-step, L = L1*L2 >= d_H, reference hankel.py:140-154):
+//       n = n2 + L2*n1, twiddle W_L^{n2*k1} between the column and row stages;
+//   * 2D (BHHB / level-2, reference block.py:136-153, fft2 over L_in x L_out):
+//       n1 = outer index, n2 = inner index, no twiddle.
+// Pipeline per batch chunk (workspace = rows of length L2, natural order):
+//   A  (k_cols)  column DFTs over n1 of h (inverse) and of each distinct x
+//                (forward), + twiddle                       -> Wh, Wx_f
+//   B  (fast 1D kernel, one "product" per row k1)           -> Wq
+//                ifft_row(Wh) .* fft_row(Wx)^p, then the transposed row DFT
+//   C  (k_cols)  + twiddle, column DFT over k1 (the transposed forward
+//                transform of the final fft), truncation    -> y
+// Zero padding and truncation are validity predicates on the loads/stores;
+// columns that carry no data (x's zero block, unused outputs) are skipped.
+#include <atomic>
+#include <stdio.h>
+
+#include "hk_fastcore.cuh"
+#include "hk_large.h"
+
+namespace hk {
+namespace large {
+
+__device__ __forceinline__ cplx tw4step(const ColArgs &a, long long e) {
+  e %= a.L;
+  const cplx hi = __ldg(&a.thi[e >> 12]);
+  const cplx lo = __ldg(&a.tlo[e & 4095]);
+  return cmul(hi, lo);
+}
+
+template <class PL, int TILE, int STAGE>
+__global__ void __launch_bounds__(TILE * PL::T, 1) k_cols(const __grid_constant__ ColArgs a) {
+  constexpr int L1 = PL::L, T = PL::T, V = PL::V, RL = PL::Rlast, R0 = PL::radix[0];
+  constexpr int PAD = TILE >= 8 ? 1 : 8 / TILE;
+  constexpr int CS = L1 + PAD;  // column stride in smem (elements)
+  constexpr bool INV = STAGE == ST_A_INV;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  cplx *tile = reinterpret_cast<cplx *>(smem_raw);
+  const int c = threadIdx.x / T, t = threadIdx.x - (threadIdx.x / T) * T;
+  const long long item = blockIdx.y;
+  const int c0 = blockIdx.x * TILE;
+
+  // ---- 1. coalesced tile load: rows n1 (or k1), TILE consecutive columns n2
+  for (int idx = threadIdx.x; idx < TILE * L1; idx += TILE * T) {
+    // operand order: columns fastest (rows contiguous in memory) or rows fastest
+    const int cc = a.in_n1_fast ? idx / L1 : idx % TILE;
+    const int n1 = a.in_n1_fast ? idx - (idx / L1) * L1 : idx / TILE;
+    const int n2 = c0 + cc;
+    cplx v = make_double2(0.0, 0.0);
+    bool ok;
+    if (a.in.len >= 0)
+      ok = n2 < a.L2 && (long long)n2 + (long long)a.L2 * n1 < a.in.len;
+    else
+      ok = n1 < a.in.e1 && n2 < a.in.e2;
+    if (ok) {
+      const long long off = item * a.in.item_stride + n1 * a.in.s1 + n2 * a.in.s2;
+      if (a.in.kind == FK_F64) {
+        v.x = __ldg(static_cast<const double *>(a.in.ptr) + off) * a.in.scale;
+      } else {
+        v = __ldg(static_cast<const cplx *>(a.in.ptr) + off);
+        v.x *= a.in.scale;
+        v.y *= a.in.scale;
+      }
+      if (STAGE == ST_C && a.twiddle) v = cmul(v, tw4step(a, (long long)n2 * n1));
+    }
+    tile[cc * CS + fast::swz2(n1)] = v;  // swizzled from the start: in-place passes
+  }
+  __syncthreads();
+
+  // ---- 2. column DFT of length L1, in place
+  cplx *col = tile + c * CS;
+  const fast::Tw0Global tw0{a.ctw0, L1 / R0, R0};
+  auto s_load = [&](int, int, int pos) { return col[fast::swz2(pos)]; };
+  auto s_store = [&](int, int, int pos, cplx v) { col[fast::swz2(pos)] = v; };
+  cplx v[V];
+  auto r_store = [&](int i, int j, int, cplx x) { v[i * RL + j] = x; };
+  if constexpr (PL::P > 1) {
+    fast::pass<PL, 0, INV, false, R0, R0>(t, a.ctw, tw0, s_load, s_store);
+    sfor<PL::P - 2>([&](auto qc) {
+      constexpr int q = decltype(qc)::value + 1;
+      __syncthreads();
+      fast::pass<PL, q, INV, false, PL::radix[q], PL::radix[q]>(t, a.ctw, tw0, s_load,
+                                                               s_store);
+    });
+    __syncthreads();
+  }
+  fast::pass<PL, PL::P - 1, INV, false, RL, RL>(t, a.ctw, tw0, s_load, r_store);
+  __syncthreads();
+
+  // ---- 3. digit-reversed registers -> natural order (+ stage-A twiddle)
+  const int n2 = c0 + c;
+#pragma unroll
+  for (int i = 0; i < V / RL; ++i) {
+    const int beta = t + i * T;
+#pragma unroll
+    for (int j = 0; j < RL; ++j) {
+      const int pos = beta * RL + j;
+      int k = 0, mul = 1;
+      sfor<PL::P>([&](auto pc) {
+        constexpr int p = decltype(pc)::value;
+        constexpr int Rp = PL::radix[p], Sp = PL::stride(p);
+        k += ((pos / Sp) % Rp) * mul;
+        mul *= Rp;
+      });
+      cplx x = v[i * RL + j];
+      if (STAGE != ST_C && a.twiddle) {
+        const cplx w = tw4step(a, (long long)n2 * k);
+        x = INV ? cmulc(x, w) : cmul(x, w);
+      }
+      col[k] = x;
+    }
+  }
+  __syncthreads();
+
+  // ---- 4. coalesced tile store
+  for (int idx = threadIdx.x; idx < TILE * L1; idx += TILE * T) {
+    const int cc = idx % TILE, n1 = idx / TILE, m2 = c0 + cc;
+    bool ok;
+    if (a.out.len >= 0)
+      ok = m2 < a.L2 && (long long)m2 + (long long)a.L2 * n1 < a.out.len;
+    else
+      ok = n1 < a.out.e1 && m2 < a.out.e2;
+    if (ok)
+      static_cast<cplx *>(a.out.ptr)[item * a.out.item_stride + n1 * a.out.s1 + m2 * a.out.s2] =
+          tile[cc * CS + n1];
+  }
+}
+
+// Per-item sums of per-row partial sums (tvp_full): fixed order, deterministic.
+__global__ void k_rowsum(const cplx *__restrict__ part, long long rows, cplx *out, long long n) {
+  const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  cplx s = make_double2(0.0, 0.0);
+  for (long long r = 0; r < rows; ++r) s = cadd(s, part[b * rows + r]);
+  out[b] = s;
+}
+
+template <class PL, int TILE, int STAGE>
+static cudaError_t launch_cols_t(const ColArgs &a, long long items, int ncols,
+                                 cudaStream_t stream) {
+  constexpr int PAD = TILE >= 8 ? 1 : 8 / TILE;
+  const int smem = TILE * (PL::L + PAD) * (int)sizeof(cplx);
+  static std::atomic<unsigned long long> configured{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(configured.load() & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(k_cols<PL, TILE, STAGE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured.fetch_or(bit);
+  }
+  dim3 grid((unsigned)((ncols + TILE - 1) / TILE), (unsigned)items);
+  if (grid.x == 0 || grid.y == 0) return cudaSuccess;
+  k_cols<PL, TILE, STAGE><<<grid, TILE * PL::T, smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+template <int STAGE>
+static cudaError_t launch_cols_stage(const ColArgs &a, long long items, int ncols,
+                                     cudaStream_t stream) {
+  switch (a.L1) {
+#define HK_COL(len, TILE, ...) \
+  case len:                    \
+    return launch_cols_t<__VA_ARGS__, TILE, STAGE>(a, items, ncols, stream);
+    HK_COL(8, 64, Plan1D<8, 1, 8>)
+    HK_COL(12, 64, Plan1D<12, 1, 12>)
+    HK_COL(16, 64, Plan1D<16, 1, 16>)
+    HK_COL(24, 64, Plan1D<24, 1, 24>)
+    HK_COL(32, 64, Plan1D<32, 2, 2, 16>)
+    HK_COL(48, 64, Plan1D<48, 3, 3, 16>)
+    HK_COL(64, 32, Plan1D<64, 4, 4, 16>)
+    HK_COL(96, 32, Plan1D<96, 6, 6, 16>)
+    HK_COL(128, 32, Plan1D<128, 8, 8, 16>)
+    HK_COL(192, 16, Plan1D<192, 12, 12, 16>)
+    HK_COL(256, 16, Plan1D<256, 16, 16, 16>)
+    HK_COL(384, 16, Plan1D<384, 24, 24, 16>)
+    HK_COL(512, 8, Plan1D<512, 32, 2, 16, 16>)
+    HK_COL(768, 8, Plan1D<768, 48, 3, 16, 16>)
+    HK_COL(1024, 8, Plan1D<1024, 64, 4, 16, 16>)
+    HK_COL(1536, 4, Plan1D<1536, 96, 6, 16, 16>)
+    HK_COL(2048, 4, Plan1D<2048, 128, 8, 16, 16>)
+#undef HK_COL
+    default:
+      return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace large
+
+bool supported_col_len(long long L1) {
+  switch (L1) {
+    case 8: case 12: case 16: case 24: case 32: case 48: case 64: case 96: case 128:
+    case 192: case 256: case 384: case 512: case 768: case 1024: case 1536: case 2048:
+      return true;
+    default:
+      return false;
+  }
+}
+
+cudaError_t launch_cols(int stage, const large::ColArgs &a, long long items, int ncols,
+                        cudaStream_t stream) {
+  switch (stage) {
+    case large::ST_A_FWD: return large::launch_cols_stage<large::ST_A_FWD>(a, items, ncols, stream);
+    case large::ST_A_INV: return large::launch_cols_stage<large::ST_A_INV>(a, items, ncols, stream);
+    default: return large::launch_cols_stage<large::ST_C>(a, items, ncols, stream);
+  }
+}
+
+cudaError_t launch_rowsum(const double2 *part, long long rows, double2 *out, long long n,
+                          cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  large::k_rowsum<<<(unsigned)((n + 127) / 128), 128, 0, stream>>>(part, rows, out, n);
+  return cudaGetLastError();
+}
+
+}  // namespace hk

@@ -1,0 +1,55 @@
+// Two-level (large-L 1D four-step / 2D block) kernels: argument structs.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hk {
+namespace large {
+
+enum ColStage : int { ST_A_FWD = 0, ST_A_INV = 1, ST_C = 2 };
+
+// An operand viewed as an L1 x L2 array; element (n1, n2) of item b sits at
+// ptr + b*item_stride + n1*s1 + n2*s2 (elements).  Valid iff
+//   1D (len >= 0): n2 + L2*n1 < len      2D (len < 0): n1 < e1 && n2 < e2
+struct Op2 {
+  const void *ptr;
+  long long item_stride;
+  long long s1, s2;
+  long long len;
+  int32_t e1, e2;
+  int32_t kind;  // FK_C128 | FK_F64
+  int32_t pad;
+  double scale;
+};
+
+struct Out2 {
+  void *ptr;
+  long long item_stride;
+  long long s1, s2;
+  long long len;
+  int32_t e1, e2;
+};
+
+struct ColArgs {
+  Op2 in;
+  Out2 out;
+  int32_t L1, L2;
+  int32_t twiddle;       // 1: four-step twiddle W_L^{n2 k1} (1D mode); 0: 2D mode
+  int32_t in_n1_fast;    // tile-load order: 1 when the operand is contiguous along n1
+  long long L;           // L1 * L2
+  const double2 *thi;    // W_L^{q*4096}
+  const double2 *tlo;    // W_L^{r}, r < 4096
+  const double2 *ctw;    // column plan table W_L1^e
+  const double2 *ctw0;   // column plan first-pass table
+};
+
+}  // namespace large
+
+bool supported_col_len(long long L1);
+cudaError_t launch_cols(int stage, const large::ColArgs &a, long long items, int ncols,
+                        cudaStream_t stream);
+cudaError_t launch_rowsum(const double2 *part, long long rows, double2 *out, long long n,
+                          cudaStream_t stream);
+
+}  // namespace hk

@@ -1,0 +1,90 @@
+"""GPU parity of the two-level (large-L four-step and 2D block) kernels
+against the CPU oracle and the reference golden outputs (cfg3, cfg4)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1401_6238_b200 as P
+from oracle import hankel_oracle as O
+from paper_1401_6238_b200 import batched, workloads
+from tests.helpers import load_golden, rand_vec, strict_relerr
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+@pytest.mark.parametrize("shape", [(3000, 3000, 3000), (5000, 4000), (20000, 9000, 30),
+                                   (4096, 4096, 4096, 4096)])
+def test_large_1d_partial_and_full(shape):
+    rng = np.random.default_rng(sum(shape))
+    d = sum(shape) - len(shape) + 1
+    h = rand_vec(rng, d)
+    xs = [rand_vec(rng, n) for n in shape]
+    H = P.HankelTensor(shape, h)
+    y = H.tvp_partial(xs[1:])
+    ref = O.hankel_tvp_partial(h, shape, xs[1:])
+    assert strict_relerr(y, ref) <= TOL
+    a = H.tvp_full(xs)
+    a_ref = O.hankel_tvp_full(h, shape, xs)
+    assert abs(a - a_ref) <= TOL * abs(a_ref)
+
+
+def test_large_1d_batched_mixed_real():
+    rng = np.random.default_rng(5)
+    shape = (4000, 3000, 2000)
+    d = sum(shape) - 2
+    B = 3
+    h = rng.standard_normal((B, d))
+    x2 = rng.standard_normal((B, shape[1]))
+    x3 = rng.standard_normal((B, shape[2])) + 1j * rng.standard_normal((B, shape[2]))
+    y = batched.hankel_tvp_partial(torch.from_numpy(h).cuda(),
+                                   [torch.from_numpy(x2).cuda(), torch.from_numpy(x3).cuda()],
+                                   shape).cpu().numpy()
+    ref = np.stack([O.hankel_tvp_partial(h[b], shape, [x2[b], x3[b]]) for b in range(B)])
+    assert strict_relerr(y, ref) <= TOL
+    spec = batched.hankel_spectrum(torch.from_numpy(h).cuda(), shape)
+    y2 = batched.hankel_tvp_partial(spec, [torch.from_numpy(x2).cuda(),
+                                           torch.from_numpy(x3).cuda()], shape,
+                                    spectrum=True).cpu().numpy()
+    assert strict_relerr(y2, ref) <= TOL
+
+
+@pytest.mark.parametrize("block,outer", [((40, 40, 40), (40, 40, 40)),
+                                         ((30, 50, 20), (25, 40, 30)),
+                                         ((60, 70), (70, 60))])
+def test_block_two_level_vs_oracle(block, outer):
+    rng = np.random.default_rng(len(block) * 7 + block[0])
+    m = len(block)
+    din, dout = sum(block) - m + 1, sum(outer) - m + 1
+    Hm = rand_vec(rng, din * dout).reshape(din, dout)
+    T = P.BhhbTensor(m, block, outer, Hm)
+    assert T._two_level
+    xs = [rand_vec(rng, n * N) for n, N in zip(block, outer)]
+    assert strict_relerr(T.tvp_partial(xs[1:]), O.bhhb_tvp_partial(Hm, block, outer, xs[1:])) <= TOL
+    a_ref = O.bhhb_tvp_full(Hm, block, outer, xs)
+    assert abs(T.tvp_full(xs) - a_ref) <= TOL * abs(a_ref)
+
+
+def test_cfg4_batch_vs_golden():
+    g = load_golden("cfg4.npz")
+    H, X = workloads.cfg4()
+    H, X = H[:64], X[:64]
+    dH = torch.from_numpy(np.ascontiguousarray(H)).cuda()
+    dx = torch.from_numpy(np.ascontiguousarray(np.transpose(X, (0, 2, 1)))).cuda().reshape(64, -1)
+    y = batched.bhhb_tvp_partial(dH, [dx, dx], 3, (64,) * 3, (64,) * 3).cpu().numpy()
+    assert strict_relerr(y[0], g["y"][0]) <= TOL
+    np.testing.assert_allclose(np.linalg.norm(y, axis=1), g["norms"][:64], rtol=TOL)
+    ref = O.bhhb_tvp_partial_batch(H[:8], X[:8], (64,) * 3, (64,) * 3)
+    assert strict_relerr(y[:8], ref) <= TOL
+
+
+def test_cfg3_vs_golden():
+    g = load_golden("cfg3.npz")
+    h, x = workloads.cfg3()
+    dh = torch.from_numpy(h).cuda()[None]
+    dx = torch.from_numpy(x).cuda()[None]
+    y = batched.hankel_tvp_partial(dh, [dx, dx], (1 << 22,) * 3)[0].cpu().numpy()
+    assert strict_relerr(y[g["idx"]], g["y"]) <= TOL
+    assert abs(np.linalg.norm(y) - float(g["norm"])) <= TOL * float(g["norm"])
