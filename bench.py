@@ -179,6 +179,104 @@ def run_reference(args):
     return 0
 
 
+# ---------------------------------------------------------------- other configs
+B_ALG_CFG = {
+    "cfg1": (298 + 100 + 100) * 8,
+    "cfg2": B_ALG,
+    "cfg3": (12_582_910 + 2 * 4_194_304) * 8,
+    "cfg4": (190 * 190 + 64 * 64 + 64 * 64) * 16,
+    "cfg5": 2000 * 16 + 2000 * 5 * 16 // 25 + 5998 * 16 // (50 * 25),
+}
+
+
+def _dev_ms(torch, fn, reps, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def _relerr(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def other_configs(torch, peak):
+    """Device-resident throughput + parity spot checks for cfg1, cfg3, cfg4, cfg5."""
+    import paper_1401_6238_b200 as P
+    from paper_1401_6238_b200 import batched, workloads
+
+    golden = os.path.join(ROOT, "tests", "golden")
+    out = {}
+
+    def rec(name, units, ms, err, extra=None):
+        bps = B_ALG_CFG[name] * units / (ms * 1e-3)
+        r = {"products_per_s": units / (ms * 1e-3), "ms": ms, "units": units,
+             "bytes_alg_per_unit": B_ALG_CFG[name], "achieved_gbs": bps / 1e9,
+             "hbm_frac": bps / 1e9 / peak, "parity_rel_err": err}
+        if extra:
+            r.update(extra)
+        out[name] = r
+
+    # cfg1: single real product, latency
+    g = np.load(os.path.join(golden, "cfg1.npz"))
+    h, x = workloads.cfg1()
+    dh = torch.from_numpy(h).cuda()[None]
+    dx = torch.from_numpy(x).cuda()[None]
+    f1 = lambda: batched.hankel_tvp_partial(dh, [dx, dx], (100,) * 3)
+    ms = _dev_ms(torch, f1, 200)
+    err = _relerr(f1()[0].cpu().numpy(), g["y"])
+    Ht = P.HankelTensor((100,) * 3, h)
+    Ht.tvp_partial([x, x])
+    t0 = time.perf_counter()
+    for _ in range(200):
+        Ht.tvp_partial([x, x])
+    api_us = (time.perf_counter() - t0) / 200 * 1e6
+    rec("cfg1", 1, ms, err, {"numpy_api_us_per_call": api_us,
+                             "metric_note": "latency-bound: us per H x^2 call"})
+    # cfg3: one large real product (four-step, L = 1536 x 8192)
+    g = np.load(os.path.join(golden, "cfg3.npz"))
+    h, x = workloads.cfg3()
+    dh = torch.from_numpy(h).cuda()[None]
+    dx = torch.from_numpy(x).cuda()[None]
+    f3 = lambda: batched.hankel_tvp_partial(dh, [dx, dx], (1 << 22,) * 3)
+    ms = _dev_ms(torch, f3, 5)
+    y = f3()[0].cpu().numpy()
+    rec("cfg3", 1, ms, _relerr(y[g["idx"]], g["y"]))
+    del dh, dx
+    # cfg4: 1024 BHHB products, 2D block kernels (L = 192 x 192)
+    g = np.load(os.path.join(golden, "cfg4.npz"))
+    Hb, X = workloads.cfg4()
+    dH = torch.from_numpy(Hb).cuda()
+    dxv = torch.from_numpy(np.ascontiguousarray(np.transpose(X, (0, 2, 1)))).cuda()
+    dxv = dxv.reshape(X.shape[0], -1)
+    f4 = lambda: batched.bhhb_tvp_partial(dH, [dxv, dxv], 3, (64,) * 3, (64,) * 3)
+    ms = _dev_ms(torch, f4, 5)
+    y = f4().cpu().numpy()
+    rec("cfg4", X.shape[0], ms, _relerr(y[g["sel"]], g["y"]))
+    del dH, dxv
+    # cfg5: one HOOI iteration's products for 256 signals (25 mixed products each)
+    g = np.load(os.path.join(golden, "cfg5.npz"))
+    sig, U0, shape = workloads.cfg5(signals=256)
+    dsig = torch.from_numpy(sig).cuda()
+    dU = torch.from_numpy(np.ascontiguousarray(np.conj(U0))).cuda()[None]
+    dU = dU.expand(sig.shape[0], -1, -1).contiguous()
+    spec = batched.hankel_spectrum(dsig, shape)
+    f5 = lambda: batched.times_matrices(spec, shape, [dU, dU], spectrum=True)
+    ms = _dev_ms(torch, f5, 5)
+    T = f5()[0].cpu().numpy()
+    rec("cfg5", sig.shape[0] * 25, ms, _relerr(T[g["rows"]], g["T1_rows"]),
+        {"metric_note": "times_matrices step of one HOOI iteration (256 signals x 25 "
+                        "products, cached spectra); per-iteration SVD excluded"})
+    return out
+
+
 # ---------------------------------------------------------------- our arm
 def run_ours(args):
     import torch
@@ -292,6 +390,11 @@ def run_ours(args):
             "clocks": clk,
             "finite_output": ok,
         }
+        if world == 1 and not args.no_extras:
+            try:
+                line["configs"] = other_configs(torch, peak)
+            except Exception as exc:  # never lose the headline line
+                line["configs"] = {"error": repr(exc)}
         if world == 1 and not args.no_cpu_baseline:
             cores = host_cores()
             per_core = args.ref_products_per_core
@@ -312,8 +415,10 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--ref-products-per-core", type=int, default=96)
+    ap.add_argument("--ref-products-per-core", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the cfg1/3/4/5 side measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
