@@ -66,7 +66,8 @@ __global__ void __launch_bounds__(PL::CTA, 1) k_hankel_1d(const __grid_constant_
   for (int f = 0; f < a.nfac; ++f) {
     const Factor &fa = a.fac[f];
     cplx w[V];
-    const long long off = item_off(fa.bstride, fa.sstride, ob, os);
+    const long long off =
+        ob * fa.bstride + (a.ncombo ? (long long)a.combo_col[os][f] : os) * fa.sstride;
     if (fa.kind == FK_SPEC) {
       const cplx *sp = static_cast<const cplx *>(fa.ptr) + off;
 #pragma unroll
@@ -85,12 +86,19 @@ __global__ void __launch_bounds__(PL::CTA, 1) k_hankel_1d(const __grid_constant_
     }
   }
 
-  cplx *out = static_cast<cplx *>(a.out) + item_off(a.out_bstride, a.out_sstride, ob, os);
+  cplx *out = static_cast<cplx *>(a.out) + ob * a.out_bstride +
+              (a.ncombo ? (long long)a.combo_out[os] : os * a.out_sstride);
+  cplx *out2 = (a.ncombo && a.combo_out2[os] >= 0)
+                   ? static_cast<cplx *>(a.out) + ob * a.out_bstride + a.combo_out2[os]
+                   : nullptr;
   if (a.mode == M_PARTIAL) {
     const int n1 = a.out_len;
     const long long es = a.out_estride;
     fft_dit_final<PL>(sbuf, t, tw, acc, [&](int pos, cplx v) {
-      if (active && pos < n1) out[pos * es] = v;
+      if (active && pos < n1) {
+        out[pos * es] = v;
+        if (out2) out2[pos * es] = v;
+      }
     });
   } else if (a.mode == M_FULL) {
     cplx s = make_double2(0.0, 0.0);

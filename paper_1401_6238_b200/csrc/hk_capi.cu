@@ -843,39 +843,93 @@ int hk_times_matrices(const hk_plan *plan, hk_operand h, const void *const *mats
       return rc;
     cspec[i] = sp;
   }
-  // one launch per column combination
+  // Column combinations, at most kMaxCombos per launch.  When two matrices
+  // share their spectra (same pointer/stride/rank/length) only the
+  // non-decreasing combinations are computed and the result is stored to
+  // every permuted slot (for m = 3: T[:, j2, j3] and T[:, j3, j2]).
+  std::vector<int> share(nmats);
+  for (int i = 0; i < nmats; ++i) {
+    share[i] = i;
+    for (int k = 0; k < i; ++k)
+      if (cspec[k] == cspec[i]) {
+        share[i] = k;
+        break;
+      }
+  }
+  const bool sym2 = nmats == 2 && share[1] == 0;
   std::vector<int64_t> j(nmats, 0);
+  struct Combo {
+    int16_t col[hk::kMaxComboFac];
+    int32_t out, out2;
+  };
+  std::vector<Combo> combos;
   for (long long c = 0; c < ncombo; ++c) {
     long long rem = c;
     for (int i = nmats - 1; i >= 0; --i) {
       j[i] = rem % ranks[i];
       rem /= ranks[i];
     }
-    Args1D a = base_args(plan, batch);
-    if ((rc = set_h(plan, hs, a))) return rc;
-    a.nfac = 0;
-    for (int i = 0; i < nmats; ++i) {
-      const double2 *ptr = cspec[i] + j[i] * L;
-      bool merged = false;
-      for (int f = 0; f < a.nfac; ++f) {
-        if (a.fac[f].ptr == ptr) {
-          a.fac[f].power += 1;
-          merged = true;
-          break;
-        }
+    if (sym2 && j[1] < j[0]) continue;
+    Combo cb{};
+    for (int i = 0; i < nmats && i < hk::kMaxComboFac; ++i) cb.col[i] = (int16_t)j[i];
+    cb.out = (int32_t)c;
+    cb.out2 = (sym2 && j[1] != j[0]) ? (int32_t)(j[1] * ranks[1] + j[0]) : -1;
+    combos.push_back(cb);
+  }
+  if (nmats > hk::kMaxComboFac) {
+    // rare: more than 4 matrices -- one launch per combination
+    for (auto &cb : combos) {
+      long long rem = cb.out;
+      for (int i = nmats - 1; i >= 0; --i) {
+        j[i] = rem % ranks[i];
+        rem /= ranks[i];
       }
-      if (merged) continue;
-      Factor &f = a.fac[a.nfac++];
-      f.ptr = ptr;
+      Args1D a = base_args(plan, batch);
+      if ((rc = set_h(plan, hs, a))) return rc;
+      a.nfac = 0;
+      for (int i = 0; i < nmats; ++i) {
+        Factor &f = a.fac[a.nfac++];
+        f.ptr = cspec[i] + j[i] * L;
+        f.bstride = ranks[i] * L;
+        f.kind = hk::FK_SPEC;
+        f.len = (int32_t)L;
+        f.power = 1;
+        f.estride = 1;
+      }
+      a.mode = hk::M_PARTIAL;
+      a.out = static_cast<double2 *>(T) + cb.out;
+      a.out_bstride = t_stride;
+      a.out_estride = (int32_t)ncombo;
+      a.out_len = (int32_t)plan->sizes[0];
+      if ((rc = launch(plan, a, stream))) return rc;
+    }
+    return HK_OK;
+  }
+  for (size_t c0 = 0; c0 < combos.size(); c0 += hk::kMaxCombos) {
+    const int nc = (int)std::min<size_t>(hk::kMaxCombos, combos.size() - c0);
+    Args1D a = base_args(plan, batch * nc);
+    a.nsub = nc;
+    a.ncombo = nc;
+    if ((rc = set_h(plan, hs, a))) return rc;
+    a.nfac = nmats;
+    for (int i = 0; i < nmats; ++i) {
+      Factor &f = a.fac[i];
+      f.ptr = cspec[i];
       f.bstride = ranks[i] * L;
-      f.sstride = 0;
+      f.sstride = L;
       f.kind = hk::FK_SPEC;
       f.len = (int32_t)L;
       f.power = 1;
       f.estride = 1;
     }
+    for (int c = 0; c < nc; ++c) {
+      const Combo &cb = combos[c0 + c];
+      for (int i = 0; i < hk::kMaxComboFac; ++i) a.combo_col[c][i] = cb.col[i];
+      a.combo_out[c] = cb.out;
+      a.combo_out2[c] = cb.out2;
+    }
     a.mode = hk::M_PARTIAL;
-    a.out = static_cast<double2 *>(T) + c;
+    a.out = T;
     a.out_bstride = t_stride;
     a.out_estride = (int32_t)ncombo;
     a.out_len = (int32_t)plan->sizes[0];

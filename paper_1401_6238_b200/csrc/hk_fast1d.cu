@@ -89,6 +89,19 @@ __global__ void __launch_bounds__(PL::CTA, Traits<PL>::min_blocks)
     const long long ob = b / a.nsub, os = b - ob * a.nsub;
 
     cplx v[V];
+    cplx *out = static_cast<cplx *>(a.out) + ob * a.out_bstride +
+                (a.ncombo ? (long long)a.combo_out[os] : os * a.out_sstride);
+    if (a.mode == M_SPEC_F) {  // column spectra: X = fft(x~) in internal layout
+      const Factor &fa = a.fac[0];
+      const long long off = ob * fa.bstride + os * fa.sstride;
+      fft_dif<PL, false, PL::radix[0]>(sbuf, t, tw, tw0,
+                                       [&](int pos) { return load_elem(fa, off, pos, 1.0); }, v);
+      if (active) {
+#pragma unroll
+        for (int r = 0; r < V; ++r) out[r * T + t] = v[r];
+      }
+      continue;
+    }
     // ---- acc = ifft(h~) (or cached spectrum) -> TMEM
     {
       const Factor &hf = a.h;
@@ -102,6 +115,13 @@ __global__ void __launch_bounds__(PL::CTA, Traits<PL>::min_blocks)
         fft_dif<PL, true, PL::radix[0]>(
             sbuf, t, tw, tw0, [&](int pos) { return load_elem(hf, off, pos, sc); }, v);
       }
+      if (a.mode == M_SPEC_H) {
+        if (active) {
+#pragma unroll
+          for (int r = 0; r < V; ++r) out[r * T + t] = v[r];
+        }
+        continue;
+      }
       tmem_wait_st();  // previous product's final reads of TMEM are complete
 #pragma unroll
       for (int c = 0; c < V / 4; ++c) tmem_st4(tmy + 16 * c, &v[4 * c]);
@@ -109,7 +129,8 @@ __global__ void __launch_bounds__(PL::CTA, Traits<PL>::min_blocks)
     // ---- acc .*= fft(x~_f)^{p_f}
     for (int f = 0; f < a.nfac; ++f) {
       const Factor &fa = a.fac[f];
-      const long long off = ob * fa.bstride + os * fa.sstride;
+      const long long off = ob * fa.bstride +
+                            (a.ncombo ? (long long)a.combo_col[os][f] : os) * fa.sstride;
       if (fa.kind == FK_SPEC) {
         const cplx *sp = static_cast<const cplx *>(fa.ptr) + off;
 #pragma unroll
@@ -134,12 +155,17 @@ __global__ void __launch_bounds__(PL::CTA, Traits<PL>::min_blocks)
 #pragma unroll
     for (int c = 0; c < V / 4; ++c) tmem_ld4(tmy + 16 * c, &v[4 * c]);
 
-    cplx *out = static_cast<cplx *>(a.out) + ob * a.out_bstride + os * a.out_sstride;
+    cplx *out2 = (a.ncombo && a.combo_out2[os] >= 0)
+                     ? static_cast<cplx *>(a.out) + ob * a.out_bstride + a.combo_out2[os]
+                     : nullptr;
     if (a.mode == M_PARTIAL) {
       const int n1 = a.out_len;
       const long long es = a.out_estride;
       fft_final<PL, NO>(sbuf, t, tw, tw0, v, [&](int pos, cplx val) {
-        if (active && pos < n1) out[pos * es] = val;
+        if (active && pos < n1) {
+          out[pos * es] = val;
+          if (out2) out2[pos * es] = val;
+        }
       });
     } else {
       cplx s = make_double2(0.0, 0.0);
@@ -256,6 +282,8 @@ struct Pruned {
 // or the request needs a mode the fast kernel does not implement.
 int fast_first_radix(long long L) {
   switch (L) {
+    case 192: return 12;
+    case 384: return 24;
     case 4096: return 16;
     case 6144: return 24;
     case 2048: return 8;
@@ -268,7 +296,7 @@ int fast_first_radix(long long L) {
 }
 
 cudaError_t launch_fast_1d(int L, const Args1D &a, cudaStream_t stream) {
-  if (a.mode != M_PARTIAL && a.mode != M_FULL) return cudaErrorNotSupported;
+
   if (!a.tw0) return cudaErrorNotSupported;
   int maxlen = 1;
   for (int f = 0; f < a.nfac; ++f)
@@ -283,6 +311,18 @@ cudaError_t launch_fast_1d(int L, const Args1D &a, cudaStream_t stream) {
     }
     case 6144: {
       using PL = Plan1D<6144, 384, 24, 16, 16>;
+      const int s0 = PL::stride(0);
+      return fast::Pruned<PL, 8, 12, 24>::launch(a, stream, (maxlen + s0 - 1) / s0,
+                                                 (outl + s0 - 1) / s0);
+    }
+    case 192: {  // BHHB rows (cfg4): x rows carry n << 192 entries, outputs n_1 << 192
+      using PL = Plan1D<192, 12, 12, 16>;
+      const int s0 = PL::stride(0);
+      return fast::Pruned<PL, 4, 6, 12>::launch(a, stream, (maxlen + s0 - 1) / s0,
+                                                (outl + s0 - 1) / s0);
+    }
+    case 384: {
+      using PL = Plan1D<384, 24, 24, 16>;
       const int s0 = PL::stride(0);
       return fast::Pruned<PL, 8, 12, 24>::launch(a, stream, (maxlen + s0 - 1) / s0,
                                                  (outl + s0 - 1) / s0);

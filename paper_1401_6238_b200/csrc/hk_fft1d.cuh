@@ -46,7 +46,15 @@ struct Plan1D {
     for (int q = 0; q <= p; ++q) s /= radix[q];
     return s;
   }
-  static constexpr int G = (T >= 256) ? 1 : 256 / T;  // independent products per CTA
+  // independent products per CTA: as many as fit 256 threads, rounded so the
+  // CTA is a whole number of warps (tcgen05 TMEM ops are warp-collective)
+  static constexpr int pick_g() {
+    if (T >= 256) return 1;
+    for (int g = 256 / T; g > 1; --g)
+      if ((g * T) % 32 == 0) return g;
+    return 256 / T;
+  }
+  static constexpr int G = pick_g();
   static constexpr int CTA = G * T;
   static constexpr int SMEM_BYTES = (P > 1) ? G * L * (int)sizeof(cplx) : 16;
 };

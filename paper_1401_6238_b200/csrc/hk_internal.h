@@ -34,6 +34,8 @@ struct Factor {
 };
 
 constexpr int kMaxFactors = 32;
+constexpr int kMaxCombos = 64;     // column combinations per times_matrices launch
+constexpr int kMaxComboFac = 4;    // distinct matrix factors addressed by the table
 
 struct Args1D {
   Factor h;                 // generating vector (inverse transform) or cached spectrum
@@ -51,7 +53,14 @@ struct Args1D {
   const double2 *tw0;       // thread-major first-pass table (fast path), may be NULL
   double scale;             // 1/L for the inverse transform
   int32_t prefetch;         // fast path: L2-prefetch the next block's operands
-  int32_t pad2;
+  // times_matrices combo table (ncombo > 0): launch item q = b * ncombo + c;
+  // factor f of combo c starts at ptr + b*bstride + combo_col[c][f]*sstride,
+  // the output at out + b*out_bstride + combo_out[c] (and combo_out2[c] >= 0,
+  // the mirrored slot of a symmetric product).
+  int32_t ncombo;
+  int16_t combo_col[kMaxCombos][kMaxComboFac];
+  int32_t combo_out[kMaxCombos];
+  int32_t combo_out2[kMaxCombos];
 };
 
 // Launch the fused 1D kernel for FFT length L (must be supported).

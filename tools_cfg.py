@@ -1,0 +1,22 @@
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+from paper_1401_6238_b200 import batched, workloads
+which = sys.argv[1]
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+if which == "cfg4":
+    Hb, X = workloads.cfg4()
+    dH = torch.from_numpy(Hb).cuda()
+    dxv = torch.from_numpy(np.ascontiguousarray(np.transpose(X, (0, 2, 1)))).cuda().reshape(1024, -1)
+    f = lambda: batched.bhhb_tvp_partial(dH, [dxv, dxv], 3, (64,)*3, (64,)*3)
+elif which == "cfg3":
+    h, x = workloads.cfg3()
+    dh = torch.from_numpy(h).cuda()[None]; dx = torch.from_numpy(x).cuda()[None]
+    f = lambda: batched.hankel_tvp_partial(dh, [dx, dx], (1 << 22,)*3)
+elif which == "cfg5":
+    sig, U0, shape = workloads.cfg5(signals=256)
+    dsig = torch.from_numpy(sig).cuda()
+    dU = torch.from_numpy(np.ascontiguousarray(np.conj(U0))).cuda()[None].expand(256, -1, -1).contiguous()
+    spec = batched.hankel_spectrum(dsig, shape)
+    f = lambda: batched.times_matrices(spec, shape, [dU, dU], spectrum=True)
+for _ in range(reps): f()
+torch.cuda.synchronize()
