@@ -471,7 +471,9 @@ long long tl_per_item(const hk_plan *p) {
   return (long long)(p->order + 2) * p->L1 * p->L2 + p->L1;  // Wh, order x Wx, Wq, row sums
 }
 long long tl_chunk(const hk_plan *p, long long batch) {
-  const long long cap = std::max(1LL, (1LL << 26) / tl_per_item(p));  // 2^26 complex = 1 GiB
+  long long cap = std::max(1LL, (1LL << 26) / tl_per_item(p));  // 2^26 complex = 1 GiB
+  static const long long env_cap = getenv("HK_TL_CHUNK") ? atoll(getenv("HK_TL_CHUNK")) : 0;
+  if (env_cap > 0) cap = std::min(cap, env_cap);
   return std::max(1LL, std::min(batch, cap));
 }
 }  // namespace

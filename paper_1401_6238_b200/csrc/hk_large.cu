@@ -18,6 +18,8 @@
 #include <atomic>
 #include <stdio.h>
 
+#include <algorithm>
+
 #include "hk_fastcore.cuh"
 #include "hk_large.h"
 
@@ -31,101 +33,142 @@ __device__ __forceinline__ cplx tw4step(const ColArgs &a, long long e) {
   return cmul(hi, lo);
 }
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
+               "r"(ok ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void *src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src),
+               "r"(ok ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Persistent column-tile kernel.  Tile w = (item, column block); the CTA keeps
+// two smem tile buffers and streams tile w+grid in with cp.async (zero-fill
+// for padding) while it transforms tile w, so global latency overlaps math.
 template <class PL, int TILE, int STAGE>
-__global__ void __launch_bounds__(TILE * PL::T, 1) k_cols(const __grid_constant__ ColArgs a) {
+__global__ void __launch_bounds__(TILE * PL::T, 1) k_cols(const __grid_constant__ ColArgs a,
+                                                          int tiles_per_item, long long ntiles) {
   constexpr int L1 = PL::L, T = PL::T, V = PL::V, RL = PL::Rlast, R0 = PL::radix[0];
   constexpr int PAD = TILE >= 8 ? 1 : 8 / TILE;
   constexpr int CS = L1 + PAD;  // column stride in smem (elements)
+  constexpr int NT = TILE * T;
   constexpr bool INV = STAGE == ST_A_INV;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  cplx *tile = reinterpret_cast<cplx *>(smem_raw);
+  cplx *bufs = reinterpret_cast<cplx *>(smem_raw);
   const int c = threadIdx.x / T, t = threadIdx.x - (threadIdx.x / T) * T;
-  const long long item = blockIdx.y;
-  const int c0 = blockIdx.x * TILE;
+  const bool real_in = a.in.kind == FK_F64;
 
-  // ---- 1. coalesced tile load: rows n1 (or k1), TILE consecutive columns n2
-  for (int idx = threadIdx.x; idx < TILE * L1; idx += TILE * T) {
-    // operand order: columns fastest (rows contiguous in memory) or rows fastest
-    const int cc = a.in_n1_fast ? idx / L1 : idx % TILE;
-    const int n1 = a.in_n1_fast ? idx - (idx / L1) * L1 : idx / TILE;
-    const int n2 = c0 + cc;
-    cplx v = make_double2(0.0, 0.0);
-    bool ok;
-    if (a.in.len >= 0)
-      ok = n2 < a.L2 && (long long)n2 + (long long)a.L2 * n1 < a.in.len;
-    else
-      ok = n1 < a.in.e1 && n2 < a.in.e2;
-    if (ok) {
-      const long long off = item * a.in.item_stride + n1 * a.in.s1 + n2 * a.in.s2;
-      if (a.in.kind == FK_F64) {
-        v.x = __ldg(static_cast<const double *>(a.in.ptr) + off) * a.in.scale;
-      } else {
-        v = __ldg(static_cast<const cplx *>(a.in.ptr) + off);
-        v.x *= a.in.scale;
-        v.y *= a.in.scale;
-      }
-      if (STAGE == ST_C && a.twiddle) v = cmul(v, tw4step(a, (long long)n2 * n1));
+  auto issue = [&](long long w, cplx *tile) {
+    const long long item = w / tiles_per_item;
+    const int c0 = (int)(w - item * tiles_per_item) * TILE;
+    for (int idx = threadIdx.x; idx < TILE * L1; idx += NT) {
+      const int cc = a.in_n1_fast ? idx / L1 : idx % TILE;
+      const int n1 = a.in_n1_fast ? idx - (idx / L1) * L1 : idx / TILE;
+      const int n2 = c0 + cc;
+      bool ok;
+      if (a.in.len >= 0)
+        ok = n2 < a.L2 && (long long)n2 + (long long)a.L2 * n1 < a.in.len;
+      else
+        ok = n1 < a.in.e1 && n2 < a.in.e2;
+      const long long off = ok ? item * a.in.item_stride + n1 * a.in.s1 + n2 * a.in.s2 : 0;
+      const uint32_t dst = smem_u32(tile + cc * CS + fast::swz2(n1));
+      if (real_in)
+        cp_async8(dst, static_cast<const double *>(a.in.ptr) + off, ok);
+      else
+        cp_async16(dst, static_cast<const cplx *>(a.in.ptr) + off, ok);
     }
-    tile[cc * CS + fast::swz2(n1)] = v;  // swizzled from the start: in-place passes
-  }
-  __syncthreads();
+    cp_async_commit();
+  };
 
-  // ---- 2. column DFT of length L1, in place
-  cplx *col = tile + c * CS;
+  long long w = blockIdx.x;
+  if (w < ntiles) issue(w, bufs);
   const fast::Tw0Global tw0{a.ctw0, L1 / R0, R0};
-  auto s_load = [&](int, int, int pos) { return col[fast::swz2(pos)]; };
-  auto s_store = [&](int, int, int pos, cplx v) { col[fast::swz2(pos)] = v; };
-  cplx v[V];
-  auto r_store = [&](int i, int j, int, cplx x) { v[i * RL + j] = x; };
-  if constexpr (PL::P > 1) {
-    fast::pass<PL, 0, INV, false, R0, R0>(t, a.ctw, tw0, s_load, s_store);
-    sfor<PL::P - 2>([&](auto qc) {
-      constexpr int q = decltype(qc)::value + 1;
-      __syncthreads();
-      fast::pass<PL, q, INV, false, PL::radix[q], PL::radix[q]>(t, a.ctw, tw0, s_load,
-                                                               s_store);
-    });
-    __syncthreads();
-  }
-  fast::pass<PL, PL::P - 1, INV, false, RL, RL>(t, a.ctw, tw0, s_load, r_store);
-  __syncthreads();
-
-  // ---- 3. digit-reversed registers -> natural order (+ stage-A twiddle)
-  const int n2 = c0 + c;
-#pragma unroll
-  for (int i = 0; i < V / RL; ++i) {
-    const int beta = t + i * T;
-#pragma unroll
-    for (int j = 0; j < RL; ++j) {
-      const int pos = beta * RL + j;
-      int k = 0, mul = 1;
-      sfor<PL::P>([&](auto pc) {
-        constexpr int p = decltype(pc)::value;
-        constexpr int Rp = PL::radix[p], Sp = PL::stride(p);
-        k += ((pos / Sp) % Rp) * mul;
-        mul *= Rp;
-      });
-      cplx x = v[i * RL + j];
-      if (STAGE != ST_C && a.twiddle) {
-        const cplx w = tw4step(a, (long long)n2 * k);
-        x = INV ? cmulc(x, w) : cmul(x, w);
-      }
-      col[k] = x;
+  for (int it = 0; w < ntiles; ++it, w += gridDim.x) {
+    cplx *tile = bufs + (it & 1) * (TILE * CS);
+    const long long wn = w + gridDim.x;
+    if (wn < ntiles) {
+      issue(wn, bufs + ((it + 1) & 1) * (TILE * CS));
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
-  }
-  __syncthreads();
-
-  // ---- 4. coalesced tile store
-  for (int idx = threadIdx.x; idx < TILE * L1; idx += TILE * T) {
-    const int cc = idx % TILE, n1 = idx / TILE, m2 = c0 + cc;
-    bool ok;
-    if (a.out.len >= 0)
-      ok = m2 < a.L2 && (long long)m2 + (long long)a.L2 * n1 < a.out.len;
-    else
-      ok = n1 < a.out.e1 && m2 < a.out.e2;
-    if (ok)
-      static_cast<cplx *>(a.out.ptr)[item * a.out.item_stride + n1 * a.out.s1 + m2 * a.out.s2] =
-          tile[cc * CS + n1];
+    __syncthreads();
+    const long long item = w / tiles_per_item;
+    const int c0 = (int)(w - item * tiles_per_item) * TILE;
+    const int n2 = c0 + c;
+    cplx *col = tile + c * CS;
+    // pass-0 input: scale, real promotion, stage-C twiddle
+    auto in_load = [&](int, int, int pos) {
+      cplx v = col[fast::swz2(pos)];
+      if (real_in) v.y = 0.0;
+      v.x *= a.in.scale;
+      v.y *= a.in.scale;
+      if (STAGE == ST_C && a.twiddle) v = cmul(v, tw4step(a, (long long)n2 * pos));
+      return v;
+    };
+    auto s_load = [&](int, int, int pos) { return col[fast::swz2(pos)]; };
+    auto s_store = [&](int, int, int pos, cplx v) { col[fast::swz2(pos)] = v; };
+    cplx v[V];
+    auto r_store = [&](int i, int j, int, cplx x) { v[i * RL + j] = x; };
+    if constexpr (PL::P > 1) {
+      fast::pass<PL, 0, INV, false, R0, R0>(t, a.ctw, tw0, in_load, s_store);
+      sfor<PL::P - 2>([&](auto qc) {
+        constexpr int q = decltype(qc)::value + 1;
+        __syncthreads();
+        fast::pass<PL, q, INV, false, PL::radix[q], PL::radix[q]>(t, a.ctw, tw0, s_load,
+                                                                 s_store);
+      });
+      __syncthreads();
+      fast::pass<PL, PL::P - 1, INV, false, RL, RL>(t, a.ctw, tw0, s_load, r_store);
+    } else {
+      fast::pass<PL, 0, INV, false, R0, R0>(t, a.ctw, tw0, in_load, r_store);
+    }
+    __syncthreads();
+    // digit-reversed registers -> natural order (+ stage-A twiddle)
+#pragma unroll
+    for (int i = 0; i < V / RL; ++i) {
+      const int beta = t + i * T;
+#pragma unroll
+      for (int j = 0; j < RL; ++j) {
+        const int pos = beta * RL + j;
+        int k = 0, mul = 1;
+        sfor<PL::P>([&](auto pc) {
+          constexpr int p = decltype(pc)::value;
+          constexpr int Rp = PL::radix[p], Sp = PL::stride(p);
+          k += ((pos / Sp) % Rp) * mul;
+          mul *= Rp;
+        });
+        cplx x = v[i * RL + j];
+        if (STAGE != ST_C && a.twiddle) {
+          const cplx tw_ = tw4step(a, (long long)n2 * k);
+          x = INV ? cmulc(x, tw_) : cmul(x, tw_);
+        }
+        col[k] = x;
+      }
+    }
+    __syncthreads();
+    // coalesced tile store
+    for (int idx = threadIdx.x; idx < TILE * L1; idx += NT) {
+      const int cc = idx % TILE, n1 = idx / TILE, m2 = c0 + cc;
+      bool ok;
+      if (a.out.len >= 0)
+        ok = m2 < a.L2 && (long long)m2 + (long long)a.L2 * n1 < a.out.len;
+      else
+        ok = n1 < a.out.e1 && m2 < a.out.e2;
+      if (ok)
+        static_cast<cplx *>(a.out.ptr)[item * a.out.item_stride + n1 * a.out.s1 +
+                                       m2 * a.out.s2] = tile[cc * CS + n1];
+    }
+    __syncthreads();  // this buffer is refilled two iterations later
   }
 }
 
@@ -142,8 +185,9 @@ template <class PL, int TILE, int STAGE>
 static cudaError_t launch_cols_t(const ColArgs &a, long long items, int ncols,
                                  cudaStream_t stream) {
   constexpr int PAD = TILE >= 8 ? 1 : 8 / TILE;
-  const int smem = TILE * (PL::L + PAD) * (int)sizeof(cplx);
+  const int smem = 2 * TILE * (PL::L + PAD) * (int)sizeof(cplx);
   static std::atomic<unsigned long long> configured{0};
+  static int resident[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
@@ -151,11 +195,29 @@ static cudaError_t launch_cols_t(const ColArgs &a, long long items, int ncols,
     cudaError_t e = cudaFuncSetAttribute(k_cols<PL, TILE, STAGE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
+    // carve out enough shared memory for every resident CTA (see resident below)
+    e = cudaFuncSetAttribute(k_cols<PL, TILE, STAGE>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_cols<PL, TILE, STAGE>);
+    int sms = 0, smem_sm = 0, regs_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+    const int nt = TILE * PL::T;
+    int per = regs_sm / (((fa.numRegs + 7) / 8 * 8) * nt);
+    per = std::min(per, smem_sm / (smem + (int)fa.sharedSizeBytes + 1024));
+    per = std::min(per, 2048 / nt);
+    resident[dev & 63] = sms * std::max(1, per);
     configured.fetch_or(bit);
   }
-  dim3 grid((unsigned)((ncols + TILE - 1) / TILE), (unsigned)items);
-  if (grid.x == 0 || grid.y == 0) return cudaSuccess;
-  k_cols<PL, TILE, STAGE><<<grid, TILE * PL::T, smem, stream>>>(a);
+  const int tiles = (ncols + TILE - 1) / TILE;
+  const long long ntiles = (long long)tiles * items;
+  if (ntiles <= 0) return cudaSuccess;
+  const long long grid = std::min<long long>(ntiles, resident[dev & 63]);
+  k_cols<PL, TILE, STAGE><<<(unsigned)grid, TILE * PL::T, smem, stream>>>(a, tiles, ntiles);
   return cudaGetLastError();
 }
 
