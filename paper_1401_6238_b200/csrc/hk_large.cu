@@ -55,7 +55,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // two smem tile buffers and streams tile w+grid in with cp.async (zero-fill
 // for padding) while it transforms tile w, so global latency overlaps math.
 template <class PL, int TILE, int STAGE>
-__global__ void __launch_bounds__(TILE * PL::T, 1) k_cols(const __grid_constant__ ColArgs a,
+__global__ void __launch_bounds__(TILE * PL::T, (TILE * PL::T <= 256) ? 2 : 1) k_cols(const __grid_constant__ ColArgs a,
                                                           int tiles_per_item, long long ntiles) {
   constexpr int L1 = PL::L, T = PL::T, V = PL::V, RL = PL::Rlast, R0 = PL::radix[0];
   constexpr int PAD = TILE >= 8 ? 1 : 8 / TILE;
