@@ -124,6 +124,8 @@ class Plan:
             self.fft_lens.append(int(L))
             lvl += 1
         self.spectrum_len = int(lib.hk_plan_spectrum_len(handle))
+        # > 0 for two-level (workspace-backed) plans
+        self.workspace_per_item = int(lib.hk_workspace_bytes(handle, 1))
 
     def __del__(self):
         try:
