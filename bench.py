@@ -283,6 +283,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_1401_6238_b200 import batched, workloads
+    from paper_1401_6238_b200.dist import max_over_ranks
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -331,12 +332,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    ms_total = t_start.elapsed_time(t_end)
-    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
-    if world > 1:
-        t = torch.tensor([ms_total], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
+    ms_total = max_over_ranks(t_start.elapsed_time(t_end), dev)
+    kern_ms = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in ev), dev)
     ms_step = ms_total / args.steps
     value = world * BATCH * args.steps / (ms_total * 1e-3)
 
@@ -357,11 +354,7 @@ def run_ours(args):
         batched.hankel_tvp_partial_host(hp, [xp, xp, xp], shape, out=yp)
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), dev)
     e2e_value = world * BATCH * e2e_steps / (e2e_ms * 1e-3)
 
     # parity spot check of this run's output (first product) against the golden norm
