@@ -25,8 +25,20 @@ def _require_cuda(t: torch.Tensor, name: str) -> None:
         raise ValueError(f"{name} must be a CUDA tensor (no CPU path exists)")
 
 
+def _physical(t: torch.Tensor) -> torch.Tensor:
+    """Materialise torch's lazy conjugate / negative bits: the kernels read raw
+    memory, and ``x.conj().contiguous()`` of a contiguous x is still a lazy view."""
+    if t.is_conj():
+        t = t.resolve_conj()
+    if t.is_neg():
+        t = t.resolve_neg()
+    return t
+
+
 def _operand(t: torch.Tensor, name: str, spectrum: bool = False) -> N.Operand:
     _require_cuda(t, name)
+    if t.is_conj() or t.is_neg():
+        raise ValueError(f"{name}: lazy conj/neg view reached the C ABI (call _physical)")
     if t.dim() != 2:
         raise ValueError(f"{name} must be 2-D (batch, length)")
     if t.stride(1) != 1:
@@ -67,6 +79,7 @@ def hankel_spectrum(h: torch.Tensor, shape, fft_len: int = 0) -> torch.Tensor:
     Returns (B, L) complex128 in the library's internal layout (opaque: only
     meaningful as the ``h`` argument of the product functions).
     """
+    h = _physical(h)
     dev = _dev_index(h)
     with torch.cuda.device(dev):
         plan = hankel_plan(shape, dev, fft_len)
@@ -76,6 +89,18 @@ def hankel_spectrum(h: torch.Tensor, shape, fft_len: int = 0) -> torch.Tensor:
         N.check(N.load_library().hk_spectrum(plan.handle, _operand(h, "h"), B, spec.data_ptr(),
                                              ws.data_ptr(), _stream(dev)), "hk_spectrum")
     return spec
+
+
+def _physical_list(ts):
+    """_physical over a list, preserving object identity of repeated entries
+    (the same tensor twice still means "same vector")."""
+    out, seen = [], {}
+    for t in ts:
+        key = id(t)
+        if key not in seen:
+            seen[key] = _physical(t)
+        out.append(seen[key])
+    return out
 
 
 def _vector_operands(xs, names):
@@ -94,7 +119,8 @@ def hankel_tvp_partial(h: torch.Tensor, xs, shape, *, spectrum: bool = False,
     """
     shape = tuple(int(n) for n in shape)
     m = len(shape)
-    xs = list(xs)
+    xs = _physical_list(xs)
+    h = _physical(h)
     if len(xs) != m - 1:
         raise ValueError(f"expected {m - 1} vectors, got {len(xs)}")
     dev = _dev_index(h)
@@ -117,7 +143,8 @@ def hankel_tvp_full(h: torch.Tensor, xs, shape, *, spectrum: bool = False,
     """alpha_b = H_b x_1 ... x_m, unconjugated (reference hankel.py:149-154). (B,) complex128."""
     shape = tuple(int(n) for n in shape)
     m = len(shape)
-    xs = list(xs)
+    xs = _physical_list(xs)
+    h = _physical(h)
     if len(xs) != m:
         raise ValueError(f"expected {m} vectors, got {len(xs)}")
     dev = _dev_index(h)
@@ -143,7 +170,8 @@ def times_matrices(h: torch.Tensor, shape, mats, *, spectrum: bool = False,
     """
     shape = tuple(int(n) for n in shape)
     m = len(shape)
-    mats = list(mats)
+    mats = _physical_list(mats)
+    h = _physical(h)
     if len(mats) != m - 1:
         raise ValueError(f"expected {m - 1} matrices, got {len(mats)}")
     dev = _dev_index(h)
@@ -194,7 +222,8 @@ def bhhb_tvp_partial(H: torch.Tensor, xs, order, block_shape, outer_shape, *,
     Returns (B, n_1 * N_1) complex128 column-stacked outputs.
     """
     block_shape, outer_shape = tuple(block_shape), tuple(outer_shape)
-    xs = list(xs)
+    xs = _physical_list(xs)
+    H = _physical(H)
     if len(xs) != order - 1:
         raise ValueError(f"expected {order - 1} vectors, got {len(xs)}")
     dev = _dev_index(H)
@@ -222,7 +251,8 @@ def bhhb_tvp_partial(H: torch.Tensor, xs, order, block_shape, outer_shape, *,
 def bhhb_tvp_full(H: torch.Tensor, xs, order, block_shape, outer_shape) -> torch.Tensor:
     """alpha_b = sum(ifft2(H_b) .* prod fft2(X~_bp)), unconjugated (block.py:146-153)."""
     block_shape, outer_shape = tuple(block_shape), tuple(outer_shape)
-    xs = list(xs)
+    xs = _physical_list(xs)
+    H = _physical(H)
     if len(xs) != order:
         raise ValueError(f"expected {order} vectors, got {len(xs)}")
     dev = _dev_index(H)

@@ -235,3 +235,20 @@ def test_cfg5_times_matrices_iteration():
     for s in range(4):
         ref = O.times_matrices_fast(sig[s], shape, [np.conj(U0)] * 2, length=6144)
         assert strict_relerr(T[s], ref) <= TOL
+
+
+def test_lazy_conj_views_are_materialised():
+    """x.conj().contiguous() of a contiguous CUDA tensor is a lazy view in torch;
+    the batched API must pass the conjugated values, not the raw storage."""
+    rng = np.random.default_rng(31)
+    shape = (50, 60, 70)
+    d = sum(shape) - 2
+    h = rng.standard_normal((2, d)) + 1j * rng.standard_normal((2, d))
+    x = rng.standard_normal((2, 60)) + 1j * rng.standard_normal((2, 60))
+    z = rng.standard_normal((2, 70)) + 1j * rng.standard_normal((2, 70))
+    dx = torch.from_numpy(x).cuda().conj().contiguous()
+    assert dx.is_conj()
+    y = batched.hankel_tvp_partial(torch.from_numpy(h).cuda(), [dx, torch.from_numpy(z).cuda()],
+                                   shape).cpu().numpy()
+    ref = np.stack([O.hankel_tvp_partial(h[b], shape, [np.conj(x[b]), z[b]]) for b in range(2)])
+    assert strict_relerr(y, ref) <= TOL
