@@ -12,7 +12,9 @@ engine on torch CUDA tensors.
 """
 
 from .block import BaabTensor, BhhbTensor, LevelKHankelTensor, unvec, vec
+from .fourier import fft1, fft2, fftn, fourier_matrix, ifft1, ifft2, ifftn
 from .hankel import DENSE_CAP, AntiCirculantTensor, HankelTensor, times_matrices
+from .hooi import TuckerResult, hooi_symmetric
 
 __version__ = "0.1.0"
 
@@ -23,6 +25,15 @@ __all__ = [
     "DENSE_CAP",
     "HankelTensor",
     "LevelKHankelTensor",
+    "TuckerResult",
+    "fft1",
+    "fft2",
+    "fftn",
+    "fourier_matrix",
+    "hooi_symmetric",
+    "ifft1",
+    "ifft2",
+    "ifftn",
     "times_matrices",
     "unvec",
     "vec",

@@ -99,3 +99,13 @@ def test_structural_helpers_without_gpu():
     np.testing.assert_array_equal(B.to_dense(), O.dense_bhhb(B.H, B.block_shape, B.outer_shape))
     pairs = P.AntiCirculantTensor(3, 3, [1, 2, 3]).special_eigenpairs()
     assert pairs[0][0] == pytest.approx(18.0)
+
+
+def test_fourier_wrappers_validate_without_gpu():
+    import paper_1401_6238_b200 as P
+
+    with pytest.raises(ValueError, match="empty input"):
+        P.fft1(np.array([]))
+    with pytest.raises(ValueError, match="size must be positive"):
+        P.fourier_matrix(0)
+    np.testing.assert_allclose(P.fourier_matrix(2), [[1, 1], [1, -1]], atol=1e-15)
