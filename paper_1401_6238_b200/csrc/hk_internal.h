@@ -57,6 +57,7 @@ struct Args1D {
   // factor f of combo c starts at ptr + b*bstride + combo_col[c][f]*sstride,
   // the output at out + b*out_bstride + combo_out[c] (and combo_out2[c] >= 0,
   // the mirrored slot of a symmetric product).
+  int32_t diag;     // diagnostics switch (0 in production)
   int32_t ncombo;
   int16_t combo_col[kMaxCombos][kMaxComboFac];
   int32_t combo_out[kMaxCombos];
@@ -71,6 +72,7 @@ cudaError_t launch_fast_1d(int L, const Args1D &a, cudaStream_t stream);
 int fast_first_radix(long long L);  // R_0 of the fast plan, 0 if none
 // Producer/consumer TMA variant (hk_pp1d.cu) for batched H x^{m-1}.
 cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream);
+
 long long choose_len_1d(long long d);  // smallest supported on-chip L >= d, or -1
 
 }  // namespace hk
