@@ -213,7 +213,8 @@ def bhhb_plan(order, block_shape, outer_shape, device: int, fft_lens=None) -> N.
 
 
 def bhhb_tvp_partial(H: torch.Tensor, xs, order, block_shape, outer_shape, *,
-                     spectrum: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
+                     spectrum: bool = False, out: torch.Tensor | None = None,
+                     fft_lens=None) -> torch.Tensor:
     """Batched BHHB product y_b = vec(fft2(ifft2(H_b) .* prod fft2(X~_bp))[:n_1, :N_1])
     (reference block.py:136-144).
 
@@ -229,7 +230,7 @@ def bhhb_tvp_partial(H: torch.Tensor, xs, order, block_shape, outer_shape, *,
     dev = _dev_index(H)
     B = H.shape[0]
     with torch.cuda.device(dev):
-        plan = bhhb_plan(order, block_shape, outer_shape, dev)
+        plan = bhhb_plan(order, block_shape, outer_shape, dev, fft_lens)
         hop, _ = _block_operand(H, "H", plan.spectrum_len if spectrum else
                                 (sum(block_shape) - order + 1) * (sum(outer_shape) - order + 1),
                                 spectrum)

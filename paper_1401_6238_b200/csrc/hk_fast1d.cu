@@ -333,8 +333,12 @@ cudaError_t launch_fast_1d(int L, const Args1D &a, cudaStream_t stream) {
       return fast::launch_variant<Plan1D<1024, 64, 4, 16, 16>, 4, 4>(a, stream);
     case 512:
       return fast::launch_variant<Plan1D<512, 32, 2, 16, 16>, 2, 2>(a, stream);
-    case 256:
-      return fast::launch_variant<Plan1D<256, 16, 16, 16>, 16, 16>(a, stream);
+    case 256: {  // BHHB rows padded to 256 (cfg4): 64 nonzero x entries, 64 outputs
+      using PL = Plan1D<256, 16, 16, 16>;
+      const int s0 = PL::stride(0);
+      return fast::Pruned<PL, 4, 8, 16>::launch(a, stream, (maxlen + s0 - 1) / s0,
+                                                (outl + s0 - 1) / s0);
+    }
     case 8192: {
       using PL = Plan1D<8192, 512, 2, 16, 16, 16>;
       return fast::launch_variant<PL, 2, 2>(a, stream);
