@@ -228,6 +228,7 @@ static cudaError_t launch_cols_stage(const ColArgs &a, long long items, int ncol
 #define HK_COL(len, TILE, ...) \
   case len:                    \
     return launch_cols_t<__VA_ARGS__, TILE, STAGE>(a, items, ncols, stream);
+    // TILE chosen so the double-buffered tile is <= ~130 KB (TILE*L1 ~ 3072 or less)
     HK_COL(8, 64, Plan1D<8, 1, 8>)
     HK_COL(12, 64, Plan1D<12, 1, 12>)
     HK_COL(16, 64, Plan1D<16, 1, 16>)
@@ -236,15 +237,15 @@ static cudaError_t launch_cols_stage(const ColArgs &a, long long items, int ncol
     HK_COL(48, 64, Plan1D<48, 3, 3, 16>)
     HK_COL(64, 32, Plan1D<64, 4, 4, 16>)
     HK_COL(96, 32, Plan1D<96, 6, 6, 16>)
-    HK_COL(128, 32, Plan1D<128, 8, 8, 16>)
+    HK_COL(128, 16, Plan1D<128, 8, 8, 16>)
     HK_COL(192, 16, Plan1D<192, 12, 12, 16>)
-    HK_COL(256, 16, Plan1D<256, 16, 16, 16>)
-    HK_COL(384, 16, Plan1D<384, 24, 24, 16>)
-    HK_COL(512, 8, Plan1D<512, 32, 2, 16, 16>)
-    HK_COL(768, 8, Plan1D<768, 48, 3, 16, 16>)
-    HK_COL(1024, 8, Plan1D<1024, 64, 4, 16, 16>)
+    HK_COL(256, 8, Plan1D<256, 16, 16, 16>)
+    HK_COL(384, 8, Plan1D<384, 24, 24, 16>)
+    HK_COL(512, 4, Plan1D<512, 32, 2, 16, 16>)
+    HK_COL(768, 4, Plan1D<768, 48, 3, 16, 16>)
+    HK_COL(1024, 2, Plan1D<1024, 64, 4, 16, 16>)
     HK_COL(1536, 4, Plan1D<1536, 96, 6, 16, 16>)
-    HK_COL(2048, 4, Plan1D<2048, 128, 8, 16, 16>)
+    HK_COL(2048, 2, Plan1D<2048, 128, 8, 16, 16>)
 #undef HK_COL
     default:
       return cudaErrorNotSupported;

@@ -88,3 +88,22 @@ def test_cfg3_vs_golden():
     y = batched.hankel_tvp_partial(dh, [dx, dx], (1 << 22,) * 3)[0].cpu().numpy()
     assert strict_relerr(y[g["idx"]], g["y"]) <= TOL
     assert abs(np.linalg.norm(y) - float(g["norm"])) <= TOL * float(g["norm"])
+
+
+@pytest.mark.parametrize("L1", [8, 12, 16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512, 768,
+                                1024, 1536, 2048])
+def test_every_column_length(L1):
+    """Two-level 1D plans forced onto each column length (fft_len = L1 * 4096)."""
+    rng = np.random.default_rng(L1)
+    L = L1 * 4096
+    n = (L - 1) // 2 + 1            # order-2 tensor with d_H <= L and > 8192
+    shape = (n // 3, L - n // 3 - 1)
+    shape = (max(1, shape[0]), max(1, min(shape[1], L // 2)))
+    d = sum(shape) - 1
+    h = rand_vec(rng, d)
+    x = rand_vec(rng, shape[1])
+    dh = torch.from_numpy(h).cuda()[None]
+    dx = torch.from_numpy(x).cuda()[None]
+    y = batched.hankel_tvp_partial(dh, [dx], shape, fft_len=L)[0].cpu().numpy()
+    ref = O.hankel_tvp_partial(h, shape, [x])
+    assert strict_relerr(y, ref) <= TOL
