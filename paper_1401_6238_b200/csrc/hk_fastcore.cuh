@@ -276,15 +276,29 @@ __device__ __forceinline__ void fft_final(cplx *sbuf, int t, const cplx *__restr
   pass<PL, 0, false, true, R0, (NO < R0 ? NO : R0)>(t, tw, tw0, s_load, g_store);
 }
 
+// Streamed operand loads bypass L1 allocation: each element is read once, and
+// keeping L1 for the twiddle tables (re-read by every pass of every product)
+// is what matters once the exchange buffer has claimed most of the carve-out.
+__device__ __forceinline__ double ld_stream(const double *p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ cplx ld_stream(const cplx *p) {
+  cplx v;
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ cplx load_elem(const Factor &f, long long off, int pos, double scale) {
   if (pos >= f.len) return make_double2(0.0, 0.0);
   const long long k = (long long)pos * f.estride;
   if (f.kind == FK_F64) {
     const double *p = static_cast<const double *>(f.ptr) + off;
-    return make_double2(__ldg(p + k) * scale, 0.0);
+    return make_double2(ld_stream(p + k) * scale, 0.0);
   }
   const cplx *p = static_cast<const cplx *>(f.ptr) + off;
-  cplx v = __ldg(p + k);
+  cplx v = ld_stream(p + k);
   return make_double2(v.x * scale, v.y * scale);
 }
 
