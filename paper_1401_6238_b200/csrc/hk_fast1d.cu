@@ -52,8 +52,40 @@ __device__ __forceinline__ void prefetch_block(const Args1D &a, long long bb, in
   }
 }
 
-template <class PL, int NZ, int NO>
-__global__ void __launch_bounds__(PL::CTA, Traits<PL>::min_blocks)
+// Plan with an explicit number of products per CTA (smaller CTAs leave room
+// for the staging slots while keeping several CTAs resident per SM).
+template <class PL, int G_>
+struct Regroup : PL {
+  static constexpr int G = G_;
+  static constexpr int CTA = G_ * PL::T;
+  static constexpr int SMEM_BYTES = G_ * PL::L * (int)sizeof(cplx);
+  static_assert(CTA % 32 == 0, "whole warps");
+};
+
+// Staging geometry: the pass-0 inputs of one thread are NB0 butterflies of R0
+// (h) or NZ (first vector factor) elements at pos = beta + j * s0.
+template <class PL, int NZ>
+struct Stage {
+  static constexpr int S0 = PL::stride(0);
+  static constexpr int NB0 = (S0 + PL::T - 1) / PL::T;
+  static constexpr int SH = NB0 * PL::radix[0];
+  static constexpr int SX = NB0 * NZ;
+  static constexpr int BYTES = (SH + SX) * PL::CTA * (int)sizeof(cplx);
+};
+
+template <class PL, bool STG>
+constexpr int min_blocks_for() {
+  return STG ? 3 : Traits<PL>::min_blocks;
+}
+
+// STG: the next item's pass-0 operands (h and the first vector factor, raw
+// c128/f64) are copied into per-thread shared-memory slots with cp.async
+// while the current item computes.  A thread only ever reads the slots it
+// filled itself, so the staging needs cp.async.wait_all and no barrier; the
+// copies for item k+1 are issued right after pass 0 of item k has consumed
+// the slots (the hook that runs behind the first exchange barrier).
+template <class PL, int NZ, int NO, bool STG = false>
+__global__ void __launch_bounds__(PL::CTA, (min_blocks_for<PL, STG>()))
     k_hankel_fast(const __grid_constant__ Args1D a) {
   using Tr = Traits<PL>;
   constexpr int T = PL::T;
@@ -76,8 +108,50 @@ __global__ void __launch_bounds__(PL::CTA, Traits<PL>::min_blocks)
   cplx *sbuf = smem + g * PL::L;
   const cplx *__restrict__ tw = a.tw;
   const Tw0Global tw0{a.tw0, PL::L / PL::radix[0], PL::radix[0]};
+  const GroupSync<PL> gsync;
   const bool do_pf = a.prefetch != 0;
   if (do_pf && threadIdx.x == 0) prefetch_block(a, blockIdx.x, PL::G);
+
+  using St = Stage<PL, NZ>;
+  constexpr int R0 = PL::radix[0];
+  const uint32_t stg = smem_u32(smem + PL::G * PL::L) + 16u * threadIdx.x;
+  auto slot = [&](int k) { return stg + (uint32_t)(k * PL::CTA * (int)sizeof(cplx)); };
+  // copy the pass-0 inputs of operand f for block bb into slots k0..
+  auto stage_issue = [&](const Factor &f, long long bb, int k0, int nin, int fac_idx) {
+    long long b = bb * PL::G + g;
+    if (b >= a.batch) b = a.batch - 1;
+    const long long ob = b / a.nsub, os = b - ob * a.nsub;
+    const long long col = (fac_idx >= 0 && a.ncombo) ? (long long)a.combo_col[os][fac_idx] : os;
+    const long long off = ob * f.bstride + col * f.sstride;
+    const bool f64 = f.kind == FK_F64;
+#pragma unroll
+    for (int i = 0; i < St::NB0; ++i) {
+      const int beta = t + i * T;
+      if (St::S0 % T == 0 || beta < St::S0) {
+#pragma unroll
+        for (int j = 0; j < nin; ++j) {
+          const int pos = beta + j * St::S0;
+          const bool ok = pos < f.len;
+          const long long e = off + (ok ? (long long)pos * f.estride : 0);
+          if (f64)
+            cpa8(slot(k0 + i * nin + j), static_cast<const double *>(f.ptr) + e, ok);
+          else
+            cpa16(slot(k0 + i * nin + j), static_cast<const cplx *>(f.ptr) + e, ok);
+        }
+      }
+    }
+  };
+  auto stage_read = [&](int k, bool f64, double sc) {
+    double x, y;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(slot(k)) : "memory");
+    if (f64) y = 0.0;
+    return make_double2(x * sc, y * sc);
+  };
+  if constexpr (STG) {
+    stage_issue(a.h, blockIdx.x, 0, R0, -1);
+    stage_issue(a.fac[0], blockIdx.x, St::SH, NZ, 0);
+    cpa_commit();
+  }
 
   // persistent loop: block bb handles products bb*G .. bb*G+G-1
   for (long long bb = blockIdx.x; bb < nblk; bb += gridDim.x) {
@@ -95,7 +169,7 @@ __global__ void __launch_bounds__(PL::CTA, Traits<PL>::min_blocks)
       const Factor &fa = a.fac[0];
       const long long off = ob * fa.bstride + os * fa.sstride;
       fft_dif<PL, false, PL::radix[0]>(sbuf, t, tw, tw0,
-                                       [&](int pos) { return load_elem(fa, off, pos, 1.0); }, v);
+                                       [&](int pos) { return load_elem(fa, off, pos, 1.0); }, v, gsync);
       if (active) {
 #pragma unroll
         for (int r = 0; r < V; ++r) out[r * T + t] = v[r];
@@ -110,10 +184,20 @@ __global__ void __launch_bounds__(PL::CTA, Traits<PL>::min_blocks)
         const cplx *sp = static_cast<const cplx *>(hf.ptr) + off;
 #pragma unroll
         for (int r = 0; r < V; ++r) v[r] = __ldg(sp + r * T + t);
+      } else if constexpr (STG) {
+        cpa_wait_all();  // this thread's copies for the current block have landed
+        const double sc = a.scale;
+        const bool f64 = hf.kind == FK_F64;
+        fft_dif<PL, true, PL::radix[0]>(
+            sbuf, t, tw, tw0,
+            [&](int i, int j, int) { return stage_read(i * R0 + j, f64, sc); }, v, gsync,
+            [&]() {
+              if (bb + gridDim.x < nblk) stage_issue(hf, bb + gridDim.x, 0, R0, -1);
+            });
       } else {
         const double sc = a.scale;
         fft_dif<PL, true, PL::radix[0]>(
-            sbuf, t, tw, tw0, [&](int pos) { return load_elem(hf, off, pos, sc); }, v);
+            sbuf, t, tw, tw0, [&](int pos) { return load_elem(hf, off, pos, sc); }, v, gsync);
       }
       if (a.mode == M_SPEC_H) {
         if (active) {
@@ -135,9 +219,18 @@ __global__ void __launch_bounds__(PL::CTA, Traits<PL>::min_blocks)
         const cplx *sp = static_cast<const cplx *>(fa.ptr) + off;
 #pragma unroll
         for (int r = 0; r < V; ++r) v[r] = __ldg(sp + r * T + t);
+      } else if (STG && f == 0) {
+        const bool f64 = fa.kind == FK_F64;
+        fft_dif<PL, false, NZ>(
+            sbuf, t, tw, tw0,
+            [&](int i, int j, int) { return stage_read(St::SH + i * NZ + j, f64, 1.0); }, v,
+            gsync, [&]() {
+              if (bb + gridDim.x < nblk) stage_issue(fa, bb + gridDim.x, St::SH, NZ, 0);
+              cpa_commit();
+            });
       } else {
         fft_dif<PL, false, NZ>(sbuf, t, tw, tw0,
-                               [&](int pos) { return load_elem(fa, off, pos, 1.0); }, v);
+                               [&](int pos) { return load_elem(fa, off, pos, 1.0); }, v, gsync);
       }
       tmem_wait_st();
 #pragma unroll
@@ -161,20 +254,23 @@ __global__ void __launch_bounds__(PL::CTA, Traits<PL>::min_blocks)
     if (a.mode == M_PARTIAL) {
       const int n1 = a.out_len;
       const long long es = a.out_estride;
-      fft_final<PL, NO>(sbuf, t, tw, tw0, v, [&](int pos, cplx val) {
-        if (active && pos < n1) {
-          out[pos * es] = val;
-          if (out2) out2[pos * es] = val;
-        }
-      });
+      fft_final<PL, NO>(
+          sbuf, t, tw, tw0, v,
+          [&](int pos, cplx val) {
+            if (active && pos < n1) {
+              out[pos * es] = val;
+              if (out2) out2[pos * es] = val;
+            }
+          },
+          gsync);
     } else {
       cplx s = make_double2(0.0, 0.0);
 #pragma unroll
       for (int r = 0; r < V; ++r) s = cadd(s, v[r]);
-      __syncthreads();
-      cplx *red = smem + g * T;
+      gsync();
+      cplx *red = sbuf;  // this group's own exchange buffer: other groups may still be mid-FFT
       red[t] = s;
-      __syncthreads();
+      gsync();
       if (t == 0 && active) {
         cplx tot = make_double2(0.0, 0.0);
         for (int k = 0; k < T; ++k) tot = cadd(tot, red[k]);
@@ -190,22 +286,22 @@ __global__ void __launch_bounds__(PL::CTA, Traits<PL>::min_blocks)
   }
 }
 
-template <class PL, int NZ, int NO>
+template <class PL, int NZ, int NO, bool STG = false>
 static cudaError_t launch_variant(const Args1D &a, cudaStream_t stream) {
-  const int smem = PL::G * PL::L * (int)sizeof(cplx) + 128;
+  const int smem = PL::G * PL::L * (int)sizeof(cplx) + (STG ? Stage<PL, NZ>::BYTES : 0) + 128;
   static std::atomic<unsigned long long> configured{0};
   int dev = 0;
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(configured.load() & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(k_hankel_fast<PL, NZ, NO>,
+    cudaError_t e = cudaFuncSetAttribute(k_hankel_fast<PL, NZ, NO, STG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     // Carve out just enough shared memory for the target residency; the rest
     // stays L1 for the twiddle tables.
-    const int want = Traits<PL>::min_blocks * (smem + 2048);
+    const int want = min_blocks_for<PL, STG>() * (smem + 2048);
     const int pct = (want * 100 + 228 * 1024 - 1) / (228 * 1024);
-    e = cudaFuncSetAttribute(k_hankel_fast<PL, NZ, NO>,
+    e = cudaFuncSetAttribute(k_hankel_fast<PL, NZ, NO, STG>,
                              cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
     if (e != cudaSuccess) return e;
     configured.fetch_or(bit);
@@ -217,11 +313,11 @@ static cudaError_t launch_variant(const Args1D &a, cudaStream_t stream) {
   if (res == 0) {
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hankel_fast<PL, NZ, NO>, PL::CTA,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hankel_fast<PL, NZ, NO, STG>, PL::CTA,
                                                   smem);
     // The occupancy API under-reports here; derive residency from the limits.
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, k_hankel_fast<PL, NZ, NO>);
+    cudaFuncGetAttributes(&fa, k_hankel_fast<PL, NZ, NO, STG>);
     int smem_sm = 0, regs_sm = 0;
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
@@ -239,7 +335,7 @@ static cudaError_t launch_variant(const Args1D &a, cudaStream_t stream) {
     }
   }
   const long long grid = nblk < res ? nblk : res;
-  k_hankel_fast<PL, NZ, NO><<<(unsigned)grid, PL::CTA, smem, stream>>>(a);
+  k_hankel_fast<PL, NZ, NO, STG><<<(unsigned)grid, PL::CTA, smem, stream>>>(a);
   return cudaGetLastError();
 }
 
@@ -263,13 +359,14 @@ struct Pruned {
       if (want <= lv[i]) return i;
     return n - 1;
   }
+  template <bool STG = false>
   static cudaError_t launch(const Args1D &a, cudaStream_t stream, int nz, int no) {
     const int zi = pick(nz), oi = pick(no);
     cudaError_t r = cudaErrorInvalidValue;
     hfor<n>([&](auto zc) {
       hfor<n>([&](auto oc) {
         constexpr int Z = decltype(zc)::value, O = decltype(oc)::value;
-        if (Z == zi && O == oi) r = launch_variant<PL, lv[Z], lv[O]>(a, stream);
+        if (Z == zi && O == oi) r = launch_variant<PL, lv[Z], lv[O], STG>(a, stream);
       });
     });
     return r;
@@ -293,6 +390,14 @@ int fast_first_radix(long long L) {
     case 8192: return 2;
     default: return 0;
   }
+}
+
+// Staged operand path: raw h and first vector factor, product modes only.
+static bool stageable(const Args1D &a) {
+  static const bool off = getenv("HK_NO_STAGE") != nullptr;
+  if (off || (a.mode != M_PARTIAL && a.mode != M_FULL) || a.nfac < 1) return false;
+  const auto raw = [](const Factor &f) { return f.kind == FK_C128 || f.kind == FK_F64; };
+  return raw(a.h) && raw(a.fac[0]);
 }
 
 cudaError_t launch_fast_1d(int L, const Args1D &a, cudaStream_t stream) {
@@ -336,8 +441,10 @@ cudaError_t launch_fast_1d(int L, const Args1D &a, cudaStream_t stream) {
     case 256: {  // BHHB rows padded to 256 (cfg4): 64 nonzero x entries, 64 outputs
       using PL = Plan1D<256, 16, 16, 16>;
       const int s0 = PL::stride(0);
-      return fast::Pruned<PL, 4, 8, 16>::launch(a, stream, (maxlen + s0 - 1) / s0,
-                                                (outl + s0 - 1) / s0);
+      const int nz = (maxlen + s0 - 1) / s0, no = (outl + s0 - 1) / s0;
+      if (stageable(a))
+        return fast::Pruned<fast::Regroup<PL, 8>, 4, 8, 16>::launch<true>(a, stream, nz, no);
+      return fast::Pruned<PL, 4, 8, 16>::launch(a, stream, nz, no);
     }
     case 8192: {
       using PL = Plan1D<8192, 512, 2, 16, 16, 16>;

@@ -3,6 +3,8 @@
 // pruned first/last passes, conflict-free swizzle.
 #pragma once
 
+#include <type_traits>
+
 #include "hk_fft1d.cuh"
 #include "hk_internal.h"
 #include "hk_tmem.cuh"
@@ -218,6 +220,18 @@ struct CtaSync {
   }
 };
 
+// When one product's threads sit inside a single warp (T <= 32, T | 32), its
+// exchanges only need the warp's lanes ordered: products in different warps
+// then run free of each other instead of in CTA lockstep.
+struct WarpSync {
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.warp.sync -1;\n" ::: "memory");
+  }
+};
+
+template <class PL>
+using GroupSync = std::conditional_t<(PL::T <= 32 && 32 % PL::T == 0), WarpSync, CtaSync>;
+
 struct NoHook {
   __device__ __forceinline__ void operator()() const {}
 };
@@ -231,7 +245,13 @@ __device__ __forceinline__ void fft_dif(cplx *sbuf, int t, const cplx *__restric
                                         Sync sync = Sync(), Hook hook = Hook()) {
   constexpr int RL = PL::Rlast;
   constexpr int R0 = PL::radix[0];
-  auto g_load = [&](int, int, int pos) { return gload(pos); };
+  // gload(pos), or gload(i, j, pos) for loaders that need the butterfly slot
+  auto g_load = [&](int i, int j, int pos) {
+    if constexpr (std::is_invocable_v<GLoad, int, int, int>)
+      return gload(i, j, pos);
+    else
+      return gload(pos);
+  };
   auto s_load_l = [&](int, int, int pos) { return sbuf[swz2(pos)]; };
   auto s_store_l = [&](int, int, int pos, cplx v) { sbuf[swz2(pos)] = v; };
   auto r_store = [&](int i, int j, int, cplx v) { out[i * RL + j] = v; };
@@ -289,6 +309,20 @@ __device__ __forceinline__ cplx ld_stream(const cplx *p) {
   asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
+
+// Per-thread asynchronous copies (LDGSTS) with zero fill past the operand end.
+__device__ __forceinline__ void cpa16(uint32_t dst, const void *src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
+               "r"(ok ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cpa8(uint32_t dst, const void *src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src),
+               "r"(ok ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 __device__ __forceinline__ cplx load_elem(const Factor &f, long long off, int pos, double scale) {
   if (pos >= f.len) return make_double2(0.0, 0.0);

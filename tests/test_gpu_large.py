@@ -53,7 +53,12 @@ def test_large_1d_batched_mixed_real():
 
 @pytest.mark.parametrize("block,outer", [((40, 40, 40), (40, 40, 40)),
                                          ((30, 50, 20), (25, 40, 30)),
-                                         ((60, 70), (70, 60))])
+                                         ((60, 70), (70, 60)),
+                                         # unequal modes / cfg4 shape: caught a reduction
+                                         # race between warp-synchronous row groups
+                                         ((60, 70), (60, 70)),
+                                         ((50, 80), (64, 64)),
+                                         ((64, 64, 64), (64, 64, 64))])
 def test_block_two_level_vs_oracle(block, outer):
     rng = np.random.default_rng(len(block) * 7 + block[0])
     m = len(block)
