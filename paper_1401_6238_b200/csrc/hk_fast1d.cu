@@ -155,6 +155,12 @@ __global__ void __launch_bounds__(PL::CTA, (min_blocks_for<PL, STG>()))
 
   // persistent loop: block bb handles products bb*G .. bb*G+G-1
   for (long long bb = blockIdx.x; bb < nblk; bb += gridDim.x) {
+    // Warp-synchronous groups never meet at a CTA barrier inside the FFTs; left
+    // alone the scheduler lets some warps run far ahead, and the kernel ends
+    // with a long tail of few resident warps.  One barrier per item bounds it.
+    if constexpr (std::is_same_v<GroupSync<PL>, WarpSync>) {
+      if (bb != blockIdx.x) __syncthreads();
+    }
     // stream the NEXT block's inputs into L2 while this one computes
     if (do_pf && threadIdx.x == 0 && bb + gridDim.x < nblk) prefetch_block(a, bb + gridDim.x, PL::G);
     long long b = bb * PL::G + g;
