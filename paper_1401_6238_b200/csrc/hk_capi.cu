@@ -31,6 +31,7 @@ struct hk_plan {
   std::vector<int64_t> L;       // per level FFT length
   const double2 *tw = nullptr;  // 1D twiddle table (length L[0])
   const double2 *tw0 = nullptr; // thread-major first-pass table for the fast kernels
+  const double2 *tw1 = nullptr; // compact W_{L/R0} table for passes >= 1 (fast kernels)
   // two-level plans (large 1D four-step or 2D block): L1 columns x L2 rows
   int two_level = 0;
   int twiddle = 0;               // 1D four-step (1) or 2D block (0)
@@ -176,12 +177,15 @@ int get_twiddles_step(int device, long long L, long long step, long long count,
 }
 
 // Tables of a length used as a row (fast / generic 1D kernel) or a column plan.
-int line_tables(int dev, long long L, const double2 **tw, const double2 **tw0) {
+int line_tables(int dev, long long L, const double2 **tw, const double2 **tw0,
+                const double2 **tw1 = nullptr) {
   int rc = get_twiddles(dev, L, tw);
   if (rc) return rc;
   const int r0 = hk::fast_first_radix(L);
   *tw0 = nullptr;
+  if (tw1) *tw1 = nullptr;
   if (r0 > 0) rc = get_twiddles0(dev, L, r0, tw0);
+  if (!rc && r0 > 0 && tw1 && L / r0 > 1) rc = get_twiddles(dev, L / r0, tw1);
   return rc;
 }
 
@@ -252,6 +256,7 @@ Args1D base_args(const hk_plan *p, int64_t batch) {
   a.nsub = 1;
   a.tw = p->tw;
   a.tw0 = p->tw0;
+  a.tw1 = p->tw1;
   a.scale = 1.0 / (double)p->L[0];
   a.out_estride = 1;
   a.prefetch = getenv("HK_NO_PREFETCH") ? 0 : 1;
@@ -341,7 +346,7 @@ int hk_plan_create_hankel(hk_plan **plan, int order, const int64_t *mode_sizes, 
   int rc = HK_OK;
   if (L > 0 && hk::supported_1d(L)) {
     p->L = {L};
-    rc = line_tables(dev, L, &p->tw, &p->tw0);
+    rc = line_tables(dev, L, &p->tw, &p->tw0, &p->tw1);
   } else {
     // two-level four-step: L = L1 * L2 (L1 column plan, L2 fast row plan)
     long long best1 = 0, best2 = 0;

@@ -112,7 +112,13 @@ struct Tw0Global {
   }
 };
 
-template <class PL, int p, bool INV, bool FINAL, int NZ, int NO, class TW0, class Load, class Store>
+// `tw` holds W_TWL^e, e in [0, TWL), TWL a multiple of every pass length
+// Lp >= 1 uses: the plan's full W_L table (TWL = L) or the compact W_{L/R0}
+// table (TWL = L / R0), whose few KB stay L1-resident next to a full
+// shared-memory carve-out (the strided reads of a W_L table touch one 128-B
+// line per twiddle).
+template <class PL, int p, bool INV, bool FINAL, int NZ, int NO, class TW0, class Load, class Store,
+          int TWL = PL::L>
 __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const TW0 &tw0,
                                      Load &&load, Store &&store) {
   using Tr = Traits<PL>;
@@ -173,7 +179,7 @@ __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const T
             cplx w[4];
             sfor<4>([&](auto qc) {
               constexpr int j = 4 * c + decltype(qc)::value + 1;
-              if constexpr (j < R) w[decltype(qc)::value] = __ldg(&tw[j * lo * (PL::L / Lp)]);
+              if constexpr (j < R) w[decltype(qc)::value] = __ldg(&tw[j * lo * (TWL / Lp)]);
             });
             sfor<4>([&](auto qc) {
               constexpr int j = 4 * c + decltype(qc)::value + 1;
@@ -238,8 +244,8 @@ struct NoHook {
 
 // hook() runs (on every thread) right after the barrier that follows pass 0,
 // i.e. once every thread of the group has consumed the pass-0 input.
-template <class PL, bool INV, int NZ, class TW0, class GLoad, class Sync = CtaSync,
-          class Hook = NoHook>
+template <class PL, bool INV, int NZ, int TWL = PL::L, class TW0, class GLoad,
+          class Sync = CtaSync, class Hook = NoHook>
 __device__ __forceinline__ void fft_dif(cplx *sbuf, int t, const cplx *__restrict__ tw,
                                         const TW0 &tw0, GLoad &&gload, cplx (&out)[PL::V],
                                         Sync sync = Sync(), Hook hook = Hook()) {
@@ -260,19 +266,24 @@ __device__ __forceinline__ void fft_dif(cplx *sbuf, int t, const cplx *__restric
   auto &&s_store = pick_io<PL>(s_store_l, sio);
   static_assert(PL::P >= 2, "fast path needs at least two passes");
   sync();
-  pass<PL, 0, INV, false, (NZ < R0 ? NZ : R0), R0>(t, tw, tw0, g_load, s_store);
+  using SL = decltype(s_load);
+  using SS = decltype(s_store);
+  pass<PL, 0, INV, false, (NZ < R0 ? NZ : R0), R0, TW0, decltype(g_load) &, SS, TWL>(
+      t, tw, tw0, g_load, s_store);
   sfor<PL::P - 2>([&](auto qc) {
     constexpr int q = decltype(qc)::value + 1;
     sync();
     if constexpr (q == 1) hook();
-    pass<PL, q, INV, false, PL::radix[q], PL::radix[q]>(t, tw, tw0, s_load, s_store);
+    pass<PL, q, INV, false, PL::radix[q], PL::radix[q], TW0, SL, SS, TWL>(t, tw, tw0, s_load,
+                                                                          s_store);
   });
   sync();
   if constexpr (PL::P == 2) hook();
-  pass<PL, PL::P - 1, INV, false, RL, RL>(t, tw, tw0, s_load, r_store);
+  pass<PL, PL::P - 1, INV, false, RL, RL, TW0, SL, decltype(r_store) &, TWL>(t, tw, tw0, s_load,
+                                                                             r_store);
 }
 
-template <class PL, int NO, class TW0, class GStore, class Sync = CtaSync>
+template <class PL, int NO, int TWL = PL::L, class TW0, class GStore, class Sync = CtaSync>
 __device__ __forceinline__ void fft_final(cplx *sbuf, int t, const cplx *__restrict__ tw,
                                           const TW0 &tw0, cplx (&in)[PL::V], GStore &&gstore,
                                           Sync sync = Sync()) {
@@ -286,14 +297,19 @@ __device__ __forceinline__ void fft_final(cplx *sbuf, int t, const cplx *__restr
   auto &&s_load = pick_io<PL>(s_load_l, sio);
   auto &&s_store = pick_io<PL>(s_store_l, sio);
   sync();
-  pass<PL, PL::P - 1, false, true, RL, RL>(t, tw, tw0, r_load, s_store);
+  using SL = decltype(s_load);
+  using SS = decltype(s_store);
+  pass<PL, PL::P - 1, false, true, RL, RL, TW0, decltype(r_load) &, SS, TWL>(t, tw, tw0, r_load,
+                                                                             s_store);
   sfor<PL::P - 2>([&](auto qc) {
     constexpr int q = PL::P - 2 - decltype(qc)::value;
     sync();
-    pass<PL, q, false, true, PL::radix[q], PL::radix[q]>(t, tw, tw0, s_load, s_store);
+    pass<PL, q, false, true, PL::radix[q], PL::radix[q], TW0, SL, SS, TWL>(t, tw, tw0, s_load,
+                                                                           s_store);
   });
   sync();
-  pass<PL, 0, false, true, R0, (NO < R0 ? NO : R0)>(t, tw, tw0, s_load, g_store);
+  pass<PL, 0, false, true, R0, (NO < R0 ? NO : R0), TW0, SL, decltype(g_store) &, TWL>(
+      t, tw, tw0, s_load, g_store);
 }
 
 // Streamed operand loads bypass L1 allocation: each element is read once, and

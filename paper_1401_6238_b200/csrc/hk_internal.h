@@ -51,6 +51,7 @@ struct Args1D {
   long long nsub;           // >= 1
   const double2 *tw;        // W_L^e, e in [0, L)
   const double2 *tw0;       // thread-major first-pass table (fast path), may be NULL
+  const double2 *tw1;       // W_{L/R0}^e, e in [0, L/R0): passes >= 1 of the fast path, may be NULL
   double scale;             // 1/L for the inverse transform
   int32_t prefetch;         // fast path: L2-prefetch the next block's operands
   // times_matrices combo table (ncombo > 0): launch item q = b * ncombo + c;

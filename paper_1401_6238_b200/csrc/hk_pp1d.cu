@@ -17,8 +17,9 @@
 // groups drift into the anti-phase that keeps the FP64 pipe busy while the
 // other group is in a barrier.
 //
-// Math per product is exactly the fast kernel's (hk_fastcore.cuh), so the
-// result is bit-identical to it.
+// Math per product is the fast kernel's (hk_fastcore.cuh) except that the
+// 1/L of the inverse transform is applied to the n_1 kept outputs instead of
+// the L inputs (4x fewer multiplies; results agree to rounding).
 #include <atomic>
 #include <stdio.h>
 #include <stdlib.h>
@@ -87,6 +88,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
   constexpr int L = PL::L, T = PL::T, V = PL::V, R0 = PL::radix[0];
   constexpr int S0 = PL::stride(0);
   constexpr int XS = NZ * S0;  // staged x elements
+  constexpr int TW1 = L / R0;  // passes >= 1 read the compact W_{L/R0} table
   (void)Layout<PL>{};
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t mbar[4];  // full_h[0..1], full_x[0..1]
@@ -100,6 +102,14 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
   const int t_in = threadIdx.x - g * T;
   const uint32_t mb_h0 = smem_u32(&mbar[0]), mb_x0 = smem_u32(&mbar[2]);
 
+  // The TMA only ever writes the first h.len (x.len) staged elements: zero the
+  // tails once so the first passes read the zero padding without bounds tests.
+  for (int i = a.h.len + (int)threadIdx.x; i < L; i += blockDim.x) hst[i] = make_double2(0.0, 0.0);
+  for (int i = a.fac[0].len + (int)threadIdx.x; i < XS; i += blockDim.x) {
+    xst[i] = make_double2(0.0, 0.0);
+    xst[XS + i] = make_double2(0.0, 0.0);
+  }
+  fence_proxy_async();
   if (warp == 0) tmem_alloc<512>(&tmem_slot);
   if (threadIdx.x == 32) {
     for (int i = 0; i < 4; ++i) mbar_init(smem_u32(&mbar[i]), 1);
@@ -170,13 +180,8 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
       // ---- S = ifft(h~) from staged h; release hst to the TMA for product k+1
       mbar_wait(mb_h0 + 8 * G, par);
       int t = fresh_t();
-      fast::fft_dif<PL, true, R0>(
-          sbuf, t, a.tw, tw0,
-          [&](int pos) {
-            if (pos >= a.h.len) return make_double2(0.0, 0.0);
-            const cplx h = hst[pos];
-            return make_double2(h.x * a.scale, h.y * a.scale);
-          },
+      fast::fft_dif<PL, true, R0, TW1>(
+          sbuf, t, a.tw1, tw0, [&](int pos) { return hst[pos]; },
           v, sync, [&]() {
             if (t == 0 && k + 1 < nloc) {
               const uint32_t mb = mb_h0 + 8 * (1 - G);
@@ -195,9 +200,8 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
       // ---- X = fft(x~) from staged x; refill this group's xst with product k+2
       mbar_wait(mb_x0 + 8 * G, par);
       t = fresh_t();
-      fast::fft_dif<PL, false, NZ>(
-          sbuf, t, a.tw, tw0,
-          [&](int pos) { return pos < a.fac[0].len ? my_x[pos] : make_double2(0.0, 0.0); }, v,
+      fast::fft_dif<PL, false, NZ, TW1>(
+          sbuf, t, a.tw1, tw0, [&](int pos) { return my_x[pos]; }, v,
           sync, [&]() {
             if (t == 0 && k + 2 < nloc) {
               const uint32_t mb = mb_x0 + 8 * G;
@@ -224,12 +228,12 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
       }
       // ---- y = fft(acc)[:n_1]
       t = fresh_t();
-      fast::fft_final<PL, NO>(
-          sbuf, t, a.tw, tw0, v,
+      fast::fft_final<PL, NO, TW1>(
+          sbuf, t, a.tw1, tw0, v,
           [&](int pos, cplx val) {
             if (pos < a.out_len)
               static_cast<cplx *>(a.out)[(blockIdx.x + k * gridDim.x) * a.out_bstride + pos] =
-                  val;
+                  make_double2(val.x * a.scale, val.y * a.scale);
           },
           sync);
     }
@@ -285,7 +289,7 @@ cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream) {
     return cudaErrorNotSupported;
   if ((reinterpret_cast<uintptr_t>(h.ptr) | reinterpret_cast<uintptr_t>(x.ptr)) & 15)
     return cudaErrorNotSupported;
-  if (h.len > L || h.len <= 0 || x.len <= 0) return cudaErrorNotSupported;
+  if (h.len > L || h.len <= 0 || x.len <= 0 || !a.tw1) return cudaErrorNotSupported;
   using PL = Plan1D<4096, 256, 16, 16, 16>;
   constexpr int s0 = PL::stride(0);
   const int nz = (x.len + s0 - 1) / s0, no = (a.out_len + s0 - 1) / s0;

@@ -3,7 +3,12 @@ sys.path.insert(0, '.')
 from paper_1401_6238_b200 import batched, workloads
 which = sys.argv[1]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-if which == "cfg4":
+if which == "cfg2":
+    h, x = workloads.cfg2()
+    dh = torch.from_numpy(h).cuda(); dx = torch.from_numpy(x).cuda()
+    y = torch.empty((4096, 1024), dtype=torch.complex128, device="cuda")
+    f = lambda: batched.hankel_tvp_partial(dh, [dx, dx, dx], (1024,)*4, out=y)
+elif which == "cfg4":
     Hb, X = workloads.cfg4()
     dH = torch.from_numpy(Hb).cuda()
     dxv = torch.from_numpy(np.ascontiguousarray(np.transpose(X, (0, 2, 1)))).cuda().reshape(1024, -1)
@@ -20,3 +25,8 @@ elif which == "cfg5":
     f = lambda: batched.times_matrices(spec, shape, [dU, dU], spectrum=True)
 for _ in range(reps): f()
 torch.cuda.synchronize()
+s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
+s.record()
+for _ in range(reps): f()
+e.record(); torch.cuda.synchronize()
+print(f"{which}: {s.elapsed_time(e) / reps * 1e3:.1f} us/step")
