@@ -95,6 +95,27 @@ struct Traits {
   static constexpr int min_blocks = (PL::CTA <= 256) ? 2 : 1;
 };
 
+// Pass-0 twiddles by recurrence: W_L^{j beta} = (W_L^beta)^j from one table
+// read per butterfly (two interleaved chains, <= 8 products deep), trading
+// 14 complex multiplies for 15 table reads (TMEM or L1 traffic).
+struct Tw0Rec {
+  const cplx *__restrict__ tw;  // W_L^e, e in [0, L)
+  __device__ __forceinline__ cplx base(int beta) const { return __ldg(&tw[beta]); }
+};
+
+template <int R, bool INV>
+__device__ __forceinline__ void twiddle_rec(cplx (&a)[R], cplx w1) {
+  const cplx w2 = cmul(w1, w1);
+  cplx wo = w1, we = w2;
+#pragma unroll
+  for (int j = 1; j < R; j += 2) {
+    a[j] = cmul_dir<INV>(a[j], wo);
+    if (j + 1 < R) a[j + 1] = cmul_dir<INV>(a[j + 1], we);
+    if (j + 2 < R) wo = cmul(wo, w2);
+    if (j + 3 < R) we = cmul(we, w2);
+  }
+}
+
 // One pass.  FINAL=false: DIF (butterfly then twiddle), pruned to NZ nonzero
 // inputs.  FINAL=true: transposed DIT of the forward transform (twiddle then
 // butterfly), pruned to NO needed outputs.
@@ -118,7 +139,7 @@ struct Tw0Global {
 // shared-memory carve-out (the strided reads of a W_L table touch one 128-B
 // line per twiddle).
 template <class PL, int p, bool INV, bool FINAL, int NZ, int NO, class TW0, class Load, class Store,
-          int TWL = PL::L>
+          int TWL = PL::L, bool REC = false>
 __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const TW0 &tw0,
                                      Load &&load, Store &&store) {
   using Tr = Traits<PL>;
@@ -159,7 +180,9 @@ __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const T
         });
       }
       auto twiddle = [&]() {
-        if constexpr (p == 0 && PL::P > 1) {
+        if constexpr (p == 0 && PL::P > 1 && std::is_same_v<TW0, Tw0Rec>) {
+          twiddle_rec<R, INV>(a, tw0.base(beta));
+        } else if constexpr (p == 0 && PL::P > 1) {
           // chunks of 4 twiddles (j = 4c+1 .. 4c+4) keep register pressure flat
           sfor<(R - 1 + 3) / 4>([&](auto cc) {
             constexpr int c = decltype(cc)::value;
@@ -170,6 +193,8 @@ __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const T
               if constexpr (j < R) a[j] = cmul_dir<INV>(a[j], w[decltype(qc)::value]);
             });
           });
+        } else if constexpr (p < PL::P - 1 && REC) {
+          twiddle_rec<R, INV>(a, __ldg(&tw[lo * (TWL / Lp)]));
         } else if constexpr (p < PL::P - 1) {
           // chunks of 4 loads behind a compiler fence: the scheduler may not
           // hoist all R-1 twiddles (4(R-1) registers) above the butterfly
@@ -244,7 +269,7 @@ struct NoHook {
 
 // hook() runs (on every thread) right after the barrier that follows pass 0,
 // i.e. once every thread of the group has consumed the pass-0 input.
-template <class PL, bool INV, int NZ, int TWL = PL::L, class TW0, class GLoad,
+template <class PL, bool INV, int NZ, int TWL = PL::L, bool REC = false, class TW0, class GLoad,
           class Sync = CtaSync, class Hook = NoHook>
 __device__ __forceinline__ void fft_dif(cplx *sbuf, int t, const cplx *__restrict__ tw,
                                         const TW0 &tw0, GLoad &&gload, cplx (&out)[PL::V],
@@ -268,22 +293,23 @@ __device__ __forceinline__ void fft_dif(cplx *sbuf, int t, const cplx *__restric
   sync();
   using SL = decltype(s_load);
   using SS = decltype(s_store);
-  pass<PL, 0, INV, false, (NZ < R0 ? NZ : R0), R0, TW0, decltype(g_load) &, SS, TWL>(
+  pass<PL, 0, INV, false, (NZ < R0 ? NZ : R0), R0, TW0, decltype(g_load) &, SS, TWL, REC>(
       t, tw, tw0, g_load, s_store);
   sfor<PL::P - 2>([&](auto qc) {
     constexpr int q = decltype(qc)::value + 1;
     sync();
     if constexpr (q == 1) hook();
-    pass<PL, q, INV, false, PL::radix[q], PL::radix[q], TW0, SL, SS, TWL>(t, tw, tw0, s_load,
+    pass<PL, q, INV, false, PL::radix[q], PL::radix[q], TW0, SL, SS, TWL, REC>(t, tw, tw0, s_load,
                                                                           s_store);
   });
   sync();
   if constexpr (PL::P == 2) hook();
-  pass<PL, PL::P - 1, INV, false, RL, RL, TW0, SL, decltype(r_store) &, TWL>(t, tw, tw0, s_load,
+  pass<PL, PL::P - 1, INV, false, RL, RL, TW0, SL, decltype(r_store) &, TWL, REC>(t, tw, tw0, s_load,
                                                                              r_store);
 }
 
-template <class PL, int NO, int TWL = PL::L, class TW0, class GStore, class Sync = CtaSync>
+template <class PL, int NO, int TWL = PL::L, bool REC = false, class TW0, class GStore,
+          class Sync = CtaSync>
 __device__ __forceinline__ void fft_final(cplx *sbuf, int t, const cplx *__restrict__ tw,
                                           const TW0 &tw0, cplx (&in)[PL::V], GStore &&gstore,
                                           Sync sync = Sync()) {
@@ -299,16 +325,16 @@ __device__ __forceinline__ void fft_final(cplx *sbuf, int t, const cplx *__restr
   sync();
   using SL = decltype(s_load);
   using SS = decltype(s_store);
-  pass<PL, PL::P - 1, false, true, RL, RL, TW0, decltype(r_load) &, SS, TWL>(t, tw, tw0, r_load,
+  pass<PL, PL::P - 1, false, true, RL, RL, TW0, decltype(r_load) &, SS, TWL, REC>(t, tw, tw0, r_load,
                                                                              s_store);
   sfor<PL::P - 2>([&](auto qc) {
     constexpr int q = PL::P - 2 - decltype(qc)::value;
     sync();
-    pass<PL, q, false, true, PL::radix[q], PL::radix[q], TW0, SL, SS, TWL>(t, tw, tw0, s_load,
+    pass<PL, q, false, true, PL::radix[q], PL::radix[q], TW0, SL, SS, TWL, REC>(t, tw, tw0, s_load,
                                                                            s_store);
   });
   sync();
-  pass<PL, 0, false, true, R0, (NO < R0 ? NO : R0), TW0, SL, decltype(g_store) &, TWL>(
+  pass<PL, 0, false, true, R0, (NO < R0 ? NO : R0), TW0, SL, decltype(g_store) &, TWL, REC>(
       t, tw, tw0, s_load, g_store);
 }
 

@@ -83,8 +83,11 @@ struct Layout {
   static_assert(PL::L / PL::radix[0] == T, "first pass: one butterfly per thread");
 };
 
-template <class PL, int NZ, int NO>
+// TWV bit 0: pass-0 twiddles by recurrence from W_L^t (else the TMEM slab);
+// bit 1: pass->=1 twiddles by recurrence from one compact-table read.
+template <class PL, int NZ, int NO, int TWV>
 __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constant__ Args1D a) {
+  constexpr bool REC = (TWV & 2) != 0;
   constexpr int L = PL::L, T = PL::T, V = PL::V, R0 = PL::radix[0];
   constexpr int S0 = PL::stride(0);
   constexpr int XS = NZ * S0;  // staged x elements
@@ -123,7 +126,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
   const uint32_t ttw = tmem_slot + lane_q + 256u + (uint32_t)((warp >> 2) * 64);
 
   // this thread's first-pass twiddles W_L^{j t} -> TMEM (same for every product)
-  {
+  if constexpr (!(TWV & 1)) {
     const fast::Tw0Global g0{a.tw0, L / R0, R0};
 #pragma unroll
     for (int c = 0; c < (R0 - 1 + 3) / 4; ++c) {
@@ -133,7 +136,12 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
     }
     tmem_wait_st();
   }
-  const Tw0Tmem tw0{ttw};
+  using TW0 = std::conditional_t<(TWV & 1) != 0, fast::Tw0Rec, Tw0Tmem>;
+  TW0 tw0;
+  if constexpr ((TWV & 1) != 0)
+    tw0 = fast::Tw0Rec{a.tw};
+  else
+    tw0 = Tw0Tmem{ttw};
 
   // Everything the loop needs is either a kernel parameter (read from the
   // constant bank at the point of use), a compile-time function of the group
@@ -180,7 +188,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
       // ---- S = ifft(h~) from staged h; release hst to the TMA for product k+1
       mbar_wait(mb_h0 + 8 * G, par);
       int t = fresh_t();
-      fast::fft_dif<PL, true, R0, TW1>(
+      fast::fft_dif<PL, true, R0, TW1, REC>(
           sbuf, t, a.tw1, tw0, [&](int pos) { return hst[pos]; },
           v, sync, [&]() {
             if (t == 0 && k + 1 < nloc) {
@@ -200,7 +208,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
       // ---- X = fft(x~) from staged x; refill this group's xst with product k+2
       mbar_wait(mb_x0 + 8 * G, par);
       t = fresh_t();
-      fast::fft_dif<PL, false, NZ, TW1>(
+      fast::fft_dif<PL, false, NZ, TW1, REC>(
           sbuf, t, a.tw1, tw0, [&](int pos) { return my_x[pos]; }, v,
           sync, [&]() {
             if (t == 0 && k + 2 < nloc) {
@@ -228,7 +236,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
       }
       // ---- y = fft(acc)[:n_1]
       t = fresh_t();
-      fast::fft_final<PL, NO, TW1>(
+      fast::fft_final<PL, NO, TW1, REC>(
           sbuf, t, a.tw1, tw0, v,
           [&](int pos, cplx val) {
             if (pos < a.out_len)
@@ -251,7 +259,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
   }
 }
 
-template <class PL, int NZ, int NO>
+template <class PL, int NZ, int NO, int TWV>
 static cudaError_t launch_pp(const Args1D &a, cudaStream_t stream) {
   constexpr int XS = NZ * PL::stride(0);
   const int smem = (3 * PL::L + 2 * XS) * (int)sizeof(cplx) + 128;
@@ -261,7 +269,7 @@ static cudaError_t launch_pp(const Args1D &a, cudaStream_t stream) {
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(configured.load() & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(k_hankel_pp<PL, NZ, NO>,
+    cudaError_t e = cudaFuncSetAttribute(k_hankel_pp<PL, NZ, NO, TWV>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
@@ -271,7 +279,7 @@ static cudaError_t launch_pp(const Args1D &a, cudaStream_t stream) {
   if (const char *e = getenv("HK_PP_GRID")) grid = atoi(e);
   if (grid > a.batch) grid = a.batch;
   if (grid <= 0) return cudaSuccess;
-  k_hankel_pp<PL, NZ, NO><<<(unsigned)grid, 2 * PL::T, smem, stream>>>(a);
+  k_hankel_pp<PL, NZ, NO, TWV><<<(unsigned)grid, 2 * PL::T, smem, stream>>>(a);
   return cudaGetLastError();
 }
 
@@ -293,7 +301,16 @@ cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream) {
   using PL = Plan1D<4096, 256, 16, 16, 16>;
   constexpr int s0 = PL::stride(0);
   const int nz = (x.len + s0 - 1) / s0, no = (a.out_len + s0 - 1) / s0;
-  if (nz <= 4 && no <= 4) return pp::launch_pp<PL, 4, 4>(a, stream);
+  int twv = 2;  // measured best on B200 (cfg2): TMEM pass 0, recurrence passes >= 1
+  if (const char *e = getenv("HK_PP_TWV")) twv = atoi(e) & 3;
+  if (nz <= 4 && no <= 4) {
+    switch (twv) {
+      case 1: return pp::launch_pp<PL, 4, 4, 1>(a, stream);
+      case 2: return pp::launch_pp<PL, 4, 4, 2>(a, stream);
+      case 3: return pp::launch_pp<PL, 4, 4, 3>(a, stream);
+      default: return pp::launch_pp<PL, 4, 4, 0>(a, stream);
+    }
+  }
   return cudaErrorNotSupported;  // x staging would not fit next to three L buffers
 }
 
