@@ -28,6 +28,10 @@
 namespace hk {
 namespace fast {
 
+// Twiddles of passes >= 1 by recurrence from one table read per butterfly
+// (fast::twiddle_rec); measured on B200 against per-twiddle L1 reads.
+constexpr bool kRec = true;
+
 // L2 prefetch (cp.async.bulk.prefetch.L2) of one operand item, if contiguous.
 __device__ __forceinline__ void prefetch_item(const Factor &f, long long b, long long nsub,
                                               int kind_bytes) {
@@ -174,7 +178,7 @@ __global__ void __launch_bounds__(PL::CTA, (min_blocks_for<PL, STG>()))
     if (a.mode == M_SPEC_F) {  // column spectra: X = fft(x~) in internal layout
       const Factor &fa = a.fac[0];
       const long long off = ob * fa.bstride + os * fa.sstride;
-      fft_dif<PL, false, PL::radix[0]>(sbuf, t, tw, tw0,
+      fft_dif<PL, false, PL::radix[0], PL::L, kRec>(sbuf, t, tw, tw0,
                                        [&](int pos) { return load_elem(fa, off, pos, 1.0); }, v, gsync);
       if (active) {
 #pragma unroll
@@ -194,7 +198,7 @@ __global__ void __launch_bounds__(PL::CTA, (min_blocks_for<PL, STG>()))
         cpa_wait_all();  // this thread's copies for the current block have landed
         const double sc = a.scale;
         const bool f64 = hf.kind == FK_F64;
-        fft_dif<PL, true, PL::radix[0]>(
+        fft_dif<PL, true, PL::radix[0], PL::L, kRec>(
             sbuf, t, tw, tw0,
             [&](int i, int j, int) { return stage_read(i * R0 + j, f64, sc); }, v, gsync,
             [&]() {
@@ -202,7 +206,7 @@ __global__ void __launch_bounds__(PL::CTA, (min_blocks_for<PL, STG>()))
             });
       } else {
         const double sc = a.scale;
-        fft_dif<PL, true, PL::radix[0]>(
+        fft_dif<PL, true, PL::radix[0], PL::L, kRec>(
             sbuf, t, tw, tw0, [&](int pos) { return load_elem(hf, off, pos, sc); }, v, gsync);
       }
       if (a.mode == M_SPEC_H) {
@@ -227,7 +231,7 @@ __global__ void __launch_bounds__(PL::CTA, (min_blocks_for<PL, STG>()))
         for (int r = 0; r < V; ++r) v[r] = __ldg(sp + r * T + t);
       } else if (STG && f == 0) {
         const bool f64 = fa.kind == FK_F64;
-        fft_dif<PL, false, NZ>(
+        fft_dif<PL, false, NZ, PL::L, kRec>(
             sbuf, t, tw, tw0,
             [&](int i, int j, int) { return stage_read(St::SH + i * NZ + j, f64, 1.0); }, v,
             gsync, [&]() {
@@ -235,7 +239,7 @@ __global__ void __launch_bounds__(PL::CTA, (min_blocks_for<PL, STG>()))
               cpa_commit();
             });
       } else {
-        fft_dif<PL, false, NZ>(sbuf, t, tw, tw0,
+        fft_dif<PL, false, NZ, PL::L, kRec>(sbuf, t, tw, tw0,
                                [&](int pos) { return load_elem(fa, off, pos, 1.0); }, v, gsync);
       }
       tmem_wait_st();
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(PL::CTA, (min_blocks_for<PL, STG>()))
     if (a.mode == M_PARTIAL) {
       const int n1 = a.out_len;
       const long long es = a.out_estride;
-      fft_final<PL, NO>(
+      fft_final<PL, NO, PL::L, kRec>(
           sbuf, t, tw, tw0, v,
           [&](int pos, cplx val) {
             if (active && pos < n1) {
