@@ -101,6 +101,18 @@ int hk_spectrum(const hk_plan *plan, hk_operand h, int64_t batch, void *spec, vo
 int hk_tvp_partial(const hk_plan *plan, hk_operand h, const hk_operand *xs, int nx,
                    int64_t batch, void *y, int64_t y_stride, void *workspace, void *stream);
 
+/* Latency form of hk_tvp_partial for ONE product with numpy-side operands
+ * (the call behind HankelTensor.tvp_partial, hankel.py:140-147, when the
+ * caller holds host arrays): copies `in_elems` complex128 values from pinned
+ * host memory `host_in` to device scratch `dev_in`, runs the product with
+ * vector p read from dev_in + x_offsets[p] (identical offsets = same vector),
+ * copies the n_1 outputs to pinned host memory `host_y` and synchronises
+ * `stream`.  h is a device operand (HK_C128 / HK_F64 / HK_SPEC).  One call
+ * replaces two copies, a launch and a sync issued separately from Python. */
+int hk_tvp_partial_host(const hk_plan *plan, hk_operand h, const void *host_in, int64_t in_elems,
+                        const int64_t *x_offsets, int nx, void *dev_in, void *dev_y,
+                        void *host_y, void *stream);
+
 /* alpha = H x_1 ... x_m (unconjugated): HankelTensor.tvp_full
  * (hankel.py:149-154) / AntiCirculantTensor.tvp_full (hankel.py:47-59).
  * xs has `order` operands.  alpha: complex128[batch] (stride 1). */

@@ -115,7 +115,7 @@ class HankelDeviceCache:
         self.h = h
         self._per_dev = {}
 
-    def _spec(self) -> tuple:
+    def _state(self) -> tuple:
         dev = require_cuda()
         st = self._per_dev.get(dev)
         if st is None:
@@ -123,19 +123,30 @@ class HankelDeviceCache:
             spec = batched.hankel_spectrum(dh, self.shape)
             st = (dh, spec)
             self._per_dev[dev] = st
+        return dev, st
+
+    def _spec(self) -> tuple:
+        dev, st = self._state()
         return dev, st[1]
 
+    # Up to this FFT length a single product runs on the latency kernel
+    # (hk_small.cu), which recomputes ifft(h~) next to the vector transforms
+    # in the same Stockham stages; it reads h itself, not the cached spectrum.
+    SMALL_L = 4096
+
     def tvp_partial(self, xs) -> np.ndarray:
-        dev, spec = self._spec()
+        dev, (dh, spec) = self._state()
         uniq, idx = _dedupe(xs)
         plan = batched.hankel_plan(self.shape, dev)
         if plan.workspace_per_item == 0:
+            if plan.fft_lens[0] <= self.SMALL_L:
+                return self._lean_partial(dev, dh, uniq, idx, N.HK_C128)
             return self._lean_partial(dev, spec, uniq, idx)
         up = _upload_packed(uniq, dev)
         y = batched.hankel_tvp_partial(spec, [up[i] for i in idx], self.shape, spectrum=True)
         return _download(y[0])
 
-    def _lean_partial(self, dev, spec, uniq, idx) -> np.ndarray:
+    def _lean_partial(self, dev, spec, uniq, idx, hkind=N.HK_SPEC) -> np.ndarray:
         """Latency path: one packed pinned H2D copy, a direct C-ABI call with
         cached plan/operand structs, one pinned D2H copy, one stream sync."""
         st = _Staging.get(dev)
@@ -149,26 +160,25 @@ class HankelDeviceCache:
             offs.append(off)
             off += a.shape[0]
         stream = torch.cuda.current_stream(dev)
-        devbuf[:n_in].copy_(host[:n_in], non_blocking=True)
         plan = batched.hankel_plan(self.shape, dev)
-        base = devbuf.data_ptr()
-        ops = (N.Operand * len(idx))()
-        for k, i in enumerate(idx):
-            ops[k] = N.Operand(base + 16 * offs[i], 0, N.HK_C128, 0)
-        hop = N.Operand(spec.data_ptr(), spec.stride(0), N.HK_SPEC, 0)
-        ybuf = devbuf[n_in:n_in + n1]
-        N.check(N.load_library().hk_tvp_partial(
-            plan.handle, hop, ops, len(idx), 1, ybuf.data_ptr(), n1, None,
-            ctypes.c_void_p(stream.cuda_stream)), "hk_tvp_partial")
-        host[n_in:n_in + n1].copy_(ybuf, non_blocking=True)
-        stream.synchronize()
+        xoff = (ctypes.c_int64 * len(idx))(*[offs[i] for i in idx])
+        hop = N.Operand(spec.data_ptr(), spec.stride(0), hkind, 0)
+        dbase, hbase = devbuf.data_ptr(), host.data_ptr()
+        # one C call: H2D of the packed vectors, the product, D2H of y, sync
+        N.check(N.load_library().hk_tvp_partial_host(
+            plan.handle, hop, hbase, n_in, xoff, len(idx), dbase, dbase + 16 * n_in,
+            hbase + 16 * n_in, ctypes.c_void_p(stream.cuda_stream)), "hk_tvp_partial_host")
         return hnp[n_in:n_in + n1].copy()
 
     def tvp_full(self, xs) -> complex:
-        dev, spec = self._spec()
+        dev, (dh, spec) = self._state()
         uniq, idx = _dedupe(xs)
         up = _upload_packed(uniq, dev)
-        a = batched.hankel_tvp_full(spec, [up[i] for i in idx], self.shape, spectrum=True)
+        plan = batched.hankel_plan(self.shape, dev)
+        if plan.workspace_per_item == 0 and plan.fft_lens[0] <= self.SMALL_L:
+            a = batched.hankel_tvp_full(dh, [up[i] for i in idx], self.shape)
+        else:
+            a = batched.hankel_tvp_full(spec, [up[i] for i in idx], self.shape, spectrum=True)
         return complex(_download(a)[0])
 
     def times_matrices(self, mats) -> np.ndarray:

@@ -50,6 +50,10 @@ _SIGS = {
     "hk_tvp_partial": (ctypes.c_int, [ctypes.c_void_p, Operand, ctypes.POINTER(Operand),
                                       ctypes.c_int, ctypes.c_int64, ctypes.c_void_p,
                                       ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
+    "hk_tvp_partial_host": (ctypes.c_int, [ctypes.c_void_p, Operand, ctypes.c_void_p,
+                                           ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
+                                           ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_void_p]),
     "hk_tvp_full": (ctypes.c_int, [ctypes.c_void_p, Operand, ctypes.POINTER(Operand),
                                    ctypes.c_int, ctypes.c_int64, ctypes.c_void_p,
                                    ctypes.c_void_p, ctypes.c_void_p]),

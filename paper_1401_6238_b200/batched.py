@@ -64,13 +64,45 @@ def hankel_plan(shape, device: int, fft_len: int = 0) -> N.Plan:
     return N.hankel_plan(shape, device, fft_len)
 
 
-def _workspace(plan: N.Plan, batch: int, device) -> torch.Tensor:
-    """Caller-owned device workspace (two-level plans; empty for on-chip plans).
+class _NoWorkspace:
+    """On-chip plans need no workspace: the C ABI receives NULL."""
+
+    @staticmethod
+    def data_ptr() -> int:
+        return 0
+
+
+def _workspace(plan: N.Plan, batch: int, device):
+    """Caller-owned device workspace (two-level plans; NULL for on-chip plans).
 
     Freed by the caching allocator after the call: the stream-ordered reuse
     rule keeps it valid for the kernels already queued on this stream."""
+    if plan.workspace_per_item == 0:
+        return _NoWorkspace
     nbytes = int(N.load_library().hk_workspace_bytes(plan.handle, batch))
     return torch.empty((max(nbytes, 16),), dtype=torch.uint8, device=device)
+
+
+class _OnDevice:
+    """``torch.cuda.device(dev)`` only when ``dev`` is not already current
+    (entering the context costs microseconds on the latency path)."""
+
+    __slots__ = ("dev", "ctx")
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.ctx = None
+
+    def __enter__(self):
+        if torch.cuda.current_device() != self.dev:
+            self.ctx = torch.cuda.device(self.dev)
+            self.ctx.__enter__()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ctx is not None:
+            self.ctx.__exit__(*exc)
+        return False
 
 
 def hankel_spectrum(h: torch.Tensor, shape, fft_len: int = 0) -> torch.Tensor:
@@ -81,7 +113,7 @@ def hankel_spectrum(h: torch.Tensor, shape, fft_len: int = 0) -> torch.Tensor:
     """
     h = _physical(h)
     dev = _dev_index(h)
-    with torch.cuda.device(dev):
+    with _OnDevice(dev):
         plan = hankel_plan(shape, dev, fft_len)
         B = h.shape[0]
         spec = torch.empty((B, plan.spectrum_len), dtype=torch.complex128, device=h.device)
@@ -125,7 +157,7 @@ def hankel_tvp_partial(h: torch.Tensor, xs, shape, *, spectrum: bool = False,
         raise ValueError(f"expected {m - 1} vectors, got {len(xs)}")
     dev = _dev_index(h)
     B = h.shape[0]
-    with torch.cuda.device(dev):
+    with _OnDevice(dev):
         plan = hankel_plan(shape, dev, fft_len)
         if out is None:
             out = torch.empty((B, shape[0]), dtype=torch.complex128, device=h.device)
@@ -149,7 +181,7 @@ def hankel_tvp_full(h: torch.Tensor, xs, shape, *, spectrum: bool = False,
         raise ValueError(f"expected {m} vectors, got {len(xs)}")
     dev = _dev_index(h)
     B = h.shape[0]
-    with torch.cuda.device(dev):
+    with _OnDevice(dev):
         plan = hankel_plan(shape, dev, fft_len)
         alpha = torch.empty((B,), dtype=torch.complex128, device=h.device)
         ops = _vector_operands(xs, [f"xs[{i}]" for i in range(len(xs))])
@@ -183,7 +215,7 @@ def times_matrices(h: torch.Tensor, shape, mats, *, spectrum: bool = False,
         if M.stride(2) != 1 or M.stride(1) != M.shape[2]:
             raise ValueError(f"matrix {p} must be row-major contiguous per item")
     ranks = [int(M.shape[2]) for M in mats]
-    with torch.cuda.device(dev):
+    with _OnDevice(dev):
         plan = hankel_plan(shape, dev, fft_len)
         lib = N.load_library()
         r_arr = N.i64_array(ranks)
@@ -229,7 +261,7 @@ def bhhb_tvp_partial(H: torch.Tensor, xs, order, block_shape, outer_shape, *,
         raise ValueError(f"expected {order - 1} vectors, got {len(xs)}")
     dev = _dev_index(H)
     B = H.shape[0]
-    with torch.cuda.device(dev):
+    with _OnDevice(dev):
         plan = bhhb_plan(order, block_shape, outer_shape, dev, fft_lens)
         hop, _ = _block_operand(H, "H", plan.spectrum_len if spectrum else
                                 (sum(block_shape) - order + 1) * (sum(outer_shape) - order + 1),
@@ -258,7 +290,7 @@ def bhhb_tvp_full(H: torch.Tensor, xs, order, block_shape, outer_shape) -> torch
         raise ValueError(f"expected {order} vectors, got {len(xs)}")
     dev = _dev_index(H)
     B = H.shape[0]
-    with torch.cuda.device(dev):
+    with _OnDevice(dev):
         plan = bhhb_plan(order, block_shape, outer_shape, dev)
         hop, _ = _block_operand(
             H, "H", (sum(block_shape) - order + 1) * (sum(outer_shape) - order + 1))

@@ -303,7 +303,9 @@ int set_vectors(const hk_plan *p, const hk_operand *xs, int nx, int mode_offset,
 
 int launch(const hk_plan *p, const Args1D &a, void *stream) {
   cudaError_t e = cudaErrorNotSupported;
-  if (!g_force_generic) e = hk::launch_pp_1d((int)p->L[0], a, (cudaStream_t)stream);
+  if (!g_force_generic) e = hk::launch_small_1d((int)p->L[0], a, (cudaStream_t)stream);
+  if (!g_force_generic && e == cudaErrorNotSupported)
+    e = hk::launch_pp_1d((int)p->L[0], a, (cudaStream_t)stream);
   if (!g_force_generic && e == cudaErrorNotSupported)
     e = hk::launch_fast_1d((int)p->L[0], a, (cudaStream_t)stream);
   if (e == cudaErrorNotSupported) e = hk::launch_1d((int)p->L[0], a, (cudaStream_t)stream);
@@ -757,6 +759,36 @@ int hk_tvp_partial(const hk_plan *plan, hk_operand h, const hk_operand *xs, int 
   a.out_bstride = y_stride;
   a.out_len = (int32_t)plan->sizes[0];
   return launch(plan, a, stream);
+}
+
+int hk_tvp_partial_host(const hk_plan *plan, hk_operand h, const void *host_in, int64_t in_elems,
+                        const int64_t *x_offsets, int nx, void *dev_in, void *dev_y,
+                        void *host_y, void *stream) {
+  int rc = check_plan(plan);
+  if (rc) return rc;
+  if (plan->two_level) return fail(HK_EUNSUPPORTED, "host latency path covers on-chip plans only");
+  if (nx != plan->order - 1)
+    return fail(HK_EINVAL, "expected %d vectors, got %d", plan->order - 1, nx);
+  if (nx > hk::kMaxFactors) return fail(HK_EUNSUPPORTED, "too many vectors");
+  if (!host_in || !dev_in || !dev_y || !host_y || !x_offsets || in_elems < 0)
+    return fail(HK_EINVAL, "NULL buffer or negative size");
+  for (int i = 0; i < nx; ++i)
+    if (x_offsets[i] < 0 || x_offsets[i] + plan->sizes[i + 1] > in_elems)
+      return fail(HK_EINVAL, "vector %d lies outside the input buffer", i);
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(dev_in, host_in, (size_t)in_elems * sizeof(double2),
+                                  cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(H2D)");
+  hk_operand xs[hk::kMaxFactors];
+  for (int i = 0; i < nx; ++i)
+    xs[i] = hk_operand{static_cast<double2 *>(dev_in) + x_offsets[i], 0, HK_C128, 0};
+  const int64_t n1 = plan->sizes[0];
+  if ((rc = hk_tvp_partial(plan, h, xs, nx, 1, dev_y, n1, nullptr, stream))) return rc;
+  e = cudaMemcpyAsync(host_y, dev_y, (size_t)n1 * sizeof(double2), cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(D2H)");
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  return HK_OK;
 }
 
 int hk_tvp_full(const hk_plan *plan, hk_operand h, const hk_operand *xs, int nx, int64_t batch,

@@ -95,6 +95,16 @@ struct Traits {
   static constexpr int min_blocks = (PL::CTA <= 256) ? 2 : 1;
 };
 
+// Pass-0 twiddle sources deliver chunks of TW0::kChunk values (default 4).
+template <class T, class = void>
+struct ChunkOf {
+  static constexpr int value = 4;
+};
+template <class T>
+struct ChunkOf<T, std::void_t<decltype(T::kChunk)>> {
+  static constexpr int value = T::kChunk;
+};
+
 // Pass-0 twiddles by recurrence: W_L^{j beta} = (W_L^beta)^j from one table
 // read per butterfly (two interleaved chains, <= 8 products deep), trading
 // 14 complex multiplies for 15 table reads (TMEM or L1 traffic).
@@ -183,13 +193,14 @@ __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const T
         if constexpr (p == 0 && PL::P > 1 && std::is_same_v<TW0, Tw0Rec>) {
           twiddle_rec<R, INV>(a, tw0.base(beta));
         } else if constexpr (p == 0 && PL::P > 1) {
-          // chunks of 4 twiddles (j = 4c+1 .. 4c+4) keep register pressure flat
-          sfor<(R - 1 + 3) / 4>([&](auto cc) {
+          // chunks of CK twiddles (j = CK*c+1 .. CK*c+CK) keep register pressure flat
+          constexpr int CK = ChunkOf<TW0>::value;
+          sfor<(R - 1 + CK - 1) / CK>([&](auto cc) {
             constexpr int c = decltype(cc)::value;
-            cplx w[4];
+            cplx w[CK];
             tw0.chunk(beta, c, w);
-            sfor<4>([&](auto qc) {
-              constexpr int j = 4 * c + decltype(qc)::value + 1;
+            sfor<CK>([&](auto qc) {
+              constexpr int j = CK * c + decltype(qc)::value + 1;
               if constexpr (j < R) a[j] = cmul_dir<INV>(a[j], w[decltype(qc)::value]);
             });
           });

@@ -73,6 +73,8 @@ cudaError_t launch_fast_1d(int L, const Args1D &a, cudaStream_t stream);
 int fast_first_radix(long long L);  // R_0 of the fast plan, 0 if none
 // Producer/consumer TMA variant (hk_pp1d.cu) for batched H x^{m-1}.
 cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream);
+// Latency kernel (hk_small.cu) for a few small direct products.
+cudaError_t launch_small_1d(int L, const Args1D &a, cudaStream_t stream);
 
 long long choose_len_1d(long long d);  // smallest supported on-chip L >= d, or -1
 

@@ -74,6 +74,12 @@ struct Tw0Tmem {
   uint32_t taddr;
   __device__ __forceinline__ void chunk(int, int c, cplx *w) const { tmem_ld4(taddr + 16 * c, w); }
 };
+// Same slab read 8 twiddles per tcgen05.ld (two waits per pass instead of four).
+struct Tw0Tmem8 {
+  static constexpr int kChunk = 8;
+  uint32_t taddr;
+  __device__ __forceinline__ void chunk(int, int c, cplx *w) const { tmem_ld8(taddr + 32 * c, w); }
+};
 
 template <class PL>
 struct Layout {
@@ -136,12 +142,13 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
     }
     tmem_wait_st();
   }
-  using TW0 = std::conditional_t<(TWV & 1) != 0, fast::Tw0Rec, Tw0Tmem>;
+  using TW0 = std::conditional_t<(TWV & 1) != 0, fast::Tw0Rec,
+                                 std::conditional_t<(TWV & 4) != 0, Tw0Tmem8, Tw0Tmem>>;
   TW0 tw0;
   if constexpr ((TWV & 1) != 0)
     tw0 = fast::Tw0Rec{a.tw};
   else
-    tw0 = Tw0Tmem{ttw};
+    tw0 = TW0{ttw};
 
   // Everything the loop needs is either a kernel parameter (read from the
   // constant bank at the point of use), a compile-time function of the group
@@ -302,9 +309,10 @@ cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream) {
   constexpr int s0 = PL::stride(0);
   const int nz = (x.len + s0 - 1) / s0, no = (a.out_len + s0 - 1) / s0;
   int twv = 2;  // measured best on B200 (cfg2): TMEM pass 0, recurrence passes >= 1
-  if (const char *e = getenv("HK_PP_TWV")) twv = atoi(e) & 3;
+  if (const char *e = getenv("HK_PP_TWV")) twv = atoi(e) & 7;
   if (nz <= 4 && no <= 4) {
     switch (twv) {
+      case 6: return pp::launch_pp<PL, 4, 4, 6>(a, stream);
       case 1: return pp::launch_pp<PL, 4, 4, 1>(a, stream);
       case 2: return pp::launch_pp<PL, 4, 4, 2>(a, stream);
       case 3: return pp::launch_pp<PL, 4, 4, 3>(a, stream);

@@ -3,7 +3,11 @@ sys.path.insert(0, '.')
 from paper_1401_6238_b200 import batched, workloads
 which = sys.argv[1]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-if which == "cfg2":
+if which == "cfg1":
+    h, x = workloads.cfg1()
+    dh = torch.from_numpy(h).cuda()[None]; dx = torch.from_numpy(x).cuda()[None]
+    f = lambda: batched.hankel_tvp_partial(dh, [dx, dx], (100,)*3)
+elif which == "cfg2":
     h, x = workloads.cfg2()
     dh = torch.from_numpy(h).cuda(); dx = torch.from_numpy(x).cuda()
     y = torch.empty((4096, 1024), dtype=torch.complex128, device="cuda")

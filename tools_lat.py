@@ -1,13 +1,22 @@
-import sys, time, numpy as np, torch
+# Where does the numpy-facing latency of HankelTensor.tvp_partial go (cfg1)?
+import sys, time, ctypes, numpy as np, torch
 sys.path.insert(0, '.')
 import paper_1401_6238_b200 as P
-from paper_1401_6238_b200 import workloads
+from paper_1401_6238_b200 import workloads, batched, _native as N, _device as D
 h, x = workloads.cfg1()
-H = P.HankelTensor((100,)*3, h)
-for _ in range(20): H.tvp_partial([x, x])
-import cProfile, pstats
-t0 = time.perf_counter()
-for _ in range(500): H.tvp_partial([x, x])
-print("us/call", (time.perf_counter() - t0) / 500 * 1e6)
-cProfile.run("for _ in range(200): H.tvp_partial([x, x])", "/tmp/prof.out")
-pstats.Stats("/tmp/prof.out").sort_stats("tottime").print_stats(12)
+H = P.HankelTensor((100,) * 3, h)
+H.tvp_partial([x, x])
+def t(fn, n=2000):
+    for _ in range(50): fn()
+    t0 = time.perf_counter()
+    for _ in range(n): fn()
+    return (time.perf_counter() - t0) / n * 1e6
+cache = H._dev if hasattr(H, "_dev") else None
+print("full API            %.1f us" % t(lambda: H.tvp_partial([x, x])))
+vecs = [H._pad(x, 1), H._pad(x, 2)]
+print("_pad x2             %.1f us" % t(lambda: [H._pad(x, 1), H._pad(x, 2)]))
+print("_partial (no pad)   %.1f us" % t(lambda: H._partial(vecs)))
+print("_dedupe             %.1f us" % t(lambda: D._dedupe(vecs)))
+print("hankel_plan         %.1f us" % t(lambda: batched.hankel_plan((100,) * 3, 0)))
+print("current_stream      %.1f us" % t(lambda: torch.cuda.current_stream(0)))
+print("cuda sync (idle)    %.1f us" % t(lambda: torch.cuda.synchronize()))
