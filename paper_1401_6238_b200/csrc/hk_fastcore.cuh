@@ -148,8 +148,8 @@ struct Tw0Global {
 // table (TWL = L / R0), whose few KB stay L1-resident next to a full
 // shared-memory carve-out (the strided reads of a W_L table touch one 128-B
 // line per twiddle).
-template <class PL, int p, bool INV, bool FINAL, int NZ, int NO, class TW0, class Load, class Store,
-          int TWL = PL::L, bool REC = false>
+template <class PL, int p, bool INV, bool FINAL, int NZ, int NO, int TWL = PL::L, bool REC = false,
+          class TW0, class Load, class Store>
 __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const TW0 &tw0,
                                      Load &&load, Store &&store) {
   using Tr = Traits<PL>;
@@ -304,18 +304,18 @@ __device__ __forceinline__ void fft_dif(cplx *sbuf, int t, const cplx *__restric
   sync();
   using SL = decltype(s_load);
   using SS = decltype(s_store);
-  pass<PL, 0, INV, false, (NZ < R0 ? NZ : R0), R0, TW0, decltype(g_load) &, SS, TWL, REC>(
+  pass<PL, 0, INV, false, (NZ < R0 ? NZ : R0), R0, TWL, REC, TW0, decltype(g_load) &, SS>(
       t, tw, tw0, g_load, s_store);
   sfor<PL::P - 2>([&](auto qc) {
     constexpr int q = decltype(qc)::value + 1;
     sync();
     if constexpr (q == 1) hook();
-    pass<PL, q, INV, false, PL::radix[q], PL::radix[q], TW0, SL, SS, TWL, REC>(t, tw, tw0, s_load,
+    pass<PL, q, INV, false, PL::radix[q], PL::radix[q], TWL, REC, TW0, SL, SS>(t, tw, tw0, s_load,
                                                                           s_store);
   });
   sync();
   if constexpr (PL::P == 2) hook();
-  pass<PL, PL::P - 1, INV, false, RL, RL, TW0, SL, decltype(r_store) &, TWL, REC>(t, tw, tw0, s_load,
+  pass<PL, PL::P - 1, INV, false, RL, RL, TWL, REC, TW0, SL, decltype(r_store) &>(t, tw, tw0, s_load,
                                                                              r_store);
 }
 
@@ -336,16 +336,16 @@ __device__ __forceinline__ void fft_final(cplx *sbuf, int t, const cplx *__restr
   sync();
   using SL = decltype(s_load);
   using SS = decltype(s_store);
-  pass<PL, PL::P - 1, false, true, RL, RL, TW0, decltype(r_load) &, SS, TWL, REC>(t, tw, tw0, r_load,
+  pass<PL, PL::P - 1, false, true, RL, RL, TWL, REC, TW0, decltype(r_load) &, SS>(t, tw, tw0, r_load,
                                                                              s_store);
   sfor<PL::P - 2>([&](auto qc) {
     constexpr int q = PL::P - 2 - decltype(qc)::value;
     sync();
-    pass<PL, q, false, true, PL::radix[q], PL::radix[q], TW0, SL, SS, TWL, REC>(t, tw, tw0, s_load,
+    pass<PL, q, false, true, PL::radix[q], PL::radix[q], TWL, REC, TW0, SL, SS>(t, tw, tw0, s_load,
                                                                            s_store);
   });
   sync();
-  pass<PL, 0, false, true, R0, (NO < R0 ? NO : R0), TW0, SL, decltype(g_store) &, TWL, REC>(
+  pass<PL, 0, false, true, R0, (NO < R0 ? NO : R0), TWL, REC, TW0, SL, decltype(g_store) &>(
       t, tw, tw0, s_load, g_store);
 }
 

@@ -26,6 +26,10 @@
 namespace hk {
 namespace large {
 
+// Column passes >= 1 take their twiddles by recurrence from one table read
+// per butterfly (fast::twiddle_rec) instead of R-1 strided table reads.
+constexpr bool kColRec = true;
+
 __device__ __forceinline__ cplx tw4step(const ColArgs &a, long long e) {
   e %= a.L;
   const cplx hi = __ldg(&a.thi[e >> 12]);
@@ -134,11 +138,11 @@ __global__ void __launch_bounds__(TILE * PL::T, (TILE * PL::T <= 256) ? 2 : 1) k
       sfor<PL::P - 2>([&](auto qc) {
         constexpr int q = decltype(qc)::value + 1;
         __syncthreads();
-        fast::pass<PL, q, INV, false, PL::radix[q], PL::radix[q]>(t, a.ctw, tw0, s_load,
+        fast::pass<PL, q, INV, false, PL::radix[q], PL::radix[q], L1, kColRec>(t, a.ctw, tw0, s_load,
                                                                  s_store);
       });
       __syncthreads();
-      fast::pass<PL, PL::P - 1, INV, false, RL, RL>(t, a.ctw, tw0, s_load, r_store);
+      fast::pass<PL, PL::P - 1, INV, false, RL, RL, L1, kColRec>(t, a.ctw, tw0, s_load, r_store);
     } else {
       fast::pass<PL, 0, INV, false, R0, R0>(t, a.ctw, tw0, in_load, r_store);
     }
