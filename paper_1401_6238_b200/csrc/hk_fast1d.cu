@@ -31,6 +31,8 @@ namespace fast {
 // Twiddles of passes >= 1 by recurrence from one table read per butterfly
 // (fast::twiddle_rec); measured on B200 against per-twiddle L1 reads.
 constexpr bool kRec = true;
+// Pass-0 twiddles by recurrence from W_L^beta (else the thread-major table).
+constexpr bool kTw0Rec = true;
 
 // L2 prefetch (cp.async.bulk.prefetch.L2) of one operand item, if contiguous.
 __device__ __forceinline__ void prefetch_item(const Factor &f, long long b, long long nsub,
@@ -111,7 +113,12 @@ __global__ void __launch_bounds__(PL::CTA, (min_blocks_for<PL, STG>()))
   const long long nblk = (a.batch + PL::G - 1) / PL::G;
   cplx *sbuf = smem + g * PL::L;
   const cplx *__restrict__ tw = a.tw;
-  const Tw0Global tw0{a.tw0, PL::L / PL::radix[0], PL::radix[0]};
+  using TW0 = std::conditional_t<kTw0Rec, Tw0Rec, Tw0Global>;
+  TW0 tw0;
+  if constexpr (kTw0Rec)
+    tw0 = Tw0Rec{a.tw};
+  else
+    tw0 = Tw0Global{a.tw0, PL::L / PL::radix[0], PL::radix[0]};
   const GroupSync<PL> gsync;
   const bool do_pf = a.prefetch != 0;
   if (do_pf && threadIdx.x == 0) prefetch_block(a, blockIdx.x, PL::G);

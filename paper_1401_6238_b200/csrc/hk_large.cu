@@ -29,6 +29,8 @@ namespace large {
 // Column passes >= 1 take their twiddles by recurrence from one table read
 // per butterfly (fast::twiddle_rec) instead of R-1 strided table reads.
 constexpr bool kColRec = true;
+// Pass-0 twiddles W_L1^{j beta} by the same recurrence from W_L1^beta.
+constexpr bool kColTw0Rec = true;
 
 __device__ __forceinline__ cplx tw4step(const ColArgs &a, long long e) {
   e %= a.L;
@@ -95,7 +97,12 @@ __global__ void __launch_bounds__(TILE * PL::T, (TILE * PL::T <= 256) ? 2 : 1) k
 
   long long w = blockIdx.x;
   if (w < ntiles) issue(w, bufs);
-  const fast::Tw0Global tw0{a.ctw0, L1 / R0, R0};
+  using TW0 = std::conditional_t<kColTw0Rec, fast::Tw0Rec, fast::Tw0Global>;
+  TW0 tw0;
+  if constexpr (kColTw0Rec)
+    tw0 = fast::Tw0Rec{a.ctw};
+  else
+    tw0 = fast::Tw0Global{a.ctw0, L1 / R0, R0};
   for (int it = 0; w < ntiles; ++it, w += gridDim.x) {
     cplx *tile = bufs + (it & 1) * (TILE * CS);
     const long long wn = w + gridDim.x;
