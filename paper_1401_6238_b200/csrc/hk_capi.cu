@@ -592,13 +592,33 @@ int tl_run(const hk_plan *p, const hk_operand &h, const hk_operand *xs, int nx, 
   } else {
     ocols = (int)p->inner[0];
   }
+  // Real h and ONE real vector (the f64 configs, e.g. cfg3): one packed
+  // column pass z = h + i x serves both (ST_A_PAIR).
+  const bool pair = p->twiddle && what != 2 && h.dtype == HK_F64 && fs.size() == 1 &&
+                    fs[0].op.dtype == HK_F64 && !getenv("HK_NO_PAIR");
   for (long long b0 = 0; b0 < batch; b0 += chunk) {
     const long long nb = std::min(chunk, batch - b0);
     cudaError_t e;
     // ---- stage A: h (inverse, 1/L applied here)
     const double2 *whp = Wh;
     long long wh_item = L;
-    if (h.dtype == HK_SPEC) {
+    int pair_xcols = 0;
+    if (pair) {
+      ca.in = hk::large::Op2{};
+      ca.in.ptr = static_cast<const char *>(h.data) + b0 * h.batch_stride * elem_bytes(h.dtype);
+      ca.in.item_stride = h.batch_stride;
+      ca.in.kind = hk::FK_F64;
+      ca.in.scale = 1.0 / (double)L;
+      ca.in.s1 = L2;
+      ca.in.s2 = 1;
+      ca.in.len = d;
+      ca.in_n1_fast = 0;
+      ca.in2 = tl_vector_op(p, fs[0].op, fs[0].mode, b0, &pair_xcols);
+      ca.out = hk::large::Out2{Wh, L, L2, 1, -1, (int32_t)L1, (int32_t)L2};
+      ca.out2 = hk::large::Out2{Wx, L, L2, 1, -1, (int32_t)L1, (int32_t)L2};
+      if ((e = hk::launch_cols(hk::large::ST_A_PAIR, ca, nb, hcols, st)) != cudaSuccess)
+        return cuda_fail(e, "column stage (h + i x)");
+    } else if (h.dtype == HK_SPEC) {
       whp = static_cast<const double2 *>(h.data) + b0 * h.batch_stride;
       wh_item = h.batch_stride;
     } else {
@@ -644,12 +664,16 @@ int tl_run(const hk_plan *p, const hk_operand &h, const hk_operand *xs, int nx, 
     a.nfac = (int)fs.size();
     for (size_t f = 0; f < fs.size(); ++f) {
       int ncols = 0;
-      ca.in = tl_vector_op(p, fs[f].op, fs[f].mode, b0, &ncols);
-      ca.in_n1_fast = 0;
       double2 *wx = Wx + (long long)f * chunk * L;
-      ca.out = hk::large::Out2{wx, L, L2, 1, -1, (int32_t)L1, (int32_t)ncols};
-      if ((e = hk::launch_cols(hk::large::ST_A_FWD, ca, nb, ncols, st)) != cudaSuccess)
-        return cuda_fail(e, "column stage (x)");
+      if (pair) {
+        ncols = pair_xcols;  // written by the packed pass above
+      } else {
+        ca.in = tl_vector_op(p, fs[f].op, fs[f].mode, b0, &ncols);
+        ca.in_n1_fast = 0;
+        ca.out = hk::large::Out2{wx, L, L2, 1, -1, (int32_t)L1, (int32_t)ncols};
+        if ((e = hk::launch_cols(hk::large::ST_A_FWD, ca, nb, ncols, st)) != cudaSuccess)
+          return cuda_fail(e, "column stage (x)");
+      }
       hk::Factor &fa = a.fac[f];
       fa.ptr = wx;
       fa.bstride = L;

@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(TILE * PL::T, (TILE * PL::T <= 256) ? 2 : 1) k
   constexpr int CS = L1 + PAD;  // column stride in smem (elements)
   constexpr int NT = TILE * T;
   constexpr bool INV = STAGE == ST_A_INV;
+  constexpr bool PAIR = STAGE == ST_A_PAIR;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   cplx *bufs = reinterpret_cast<cplx *>(smem_raw);
   const int c = threadIdx.x / T, t = threadIdx.x - (threadIdx.x / T) * T;
@@ -87,10 +88,17 @@ __global__ void __launch_bounds__(TILE * PL::T, (TILE * PL::T <= 256) ? 2 : 1) k
         ok = n1 < a.in.e1 && n2 < a.in.e2;
       const long long off = ok ? item * a.in.item_stride + n1 * a.in.s1 + n2 * a.in.s2 : 0;
       const uint32_t dst = smem_u32(tile + cc * CS + fast::swz2(n1));
-      if (real_in)
+      if constexpr (PAIR) {  // z = h + i x from two real streams (1D layout)
+        const bool ok2 = n2 < a.L2 && (long long)n2 + (long long)a.L2 * n1 < a.in2.len;
+        const long long off2 =
+            ok2 ? item * a.in2.item_stride + n1 * a.in2.s1 + n2 * a.in2.s2 : 0;
         cp_async8(dst, static_cast<const double *>(a.in.ptr) + off, ok);
-      else
+        cp_async8(dst + 8, static_cast<const double *>(a.in2.ptr) + off2, ok2);
+      } else if (real_in) {
+        cp_async8(dst, static_cast<const double *>(a.in.ptr) + off, ok);
+      } else {
         cp_async16(dst, static_cast<const cplx *>(a.in.ptr) + off, ok);
+      }
     }
     cp_async_commit();
   };
@@ -126,6 +134,7 @@ __global__ void __launch_bounds__(TILE * PL::T, (TILE * PL::T <= 256) ? 2 : 1) k
     if (STAGE == ST_C && a.twiddle) tw_step = tw4step(a, (long long)n2 * S0);
     auto in_load = [&](int, int j, int pos) {
       cplx v = col[fast::swz2(pos)];
+      if constexpr (PAIR) return v;  // scale of h applied when z is split
       if (real_in) v.y = 0.0;
       v.x *= a.in.scale;
       v.y *= a.in.scale;
@@ -157,8 +166,9 @@ __global__ void __launch_bounds__(TILE * PL::T, (TILE * PL::T <= 256) ? 2 : 1) k
     // digit-reversed registers -> natural order (+ stage-A twiddle)
     // last-pass register j of butterfly beta holds frequency k = k(beta) + j*L1/RL
     // (j is the most significant mixed-radix digit): geometric twiddles again
-    const cplx tws = (STAGE != ST_C && a.twiddle) ? tw4step(a, (long long)n2 * (L1 / RL))
-                                                  : make_double2(1.0, 0.0);
+    constexpr bool TW_A = STAGE != ST_C && !PAIR;  // stage-A twiddle in this loop
+    const cplx tws = (TW_A && a.twiddle) ? tw4step(a, (long long)n2 * (L1 / RL))
+                                         : make_double2(1.0, 0.0);
 #pragma unroll
     for (int i = 0; i < V / RL; ++i) {
       const int beta = t + i * T;
@@ -169,13 +179,13 @@ __global__ void __launch_bounds__(TILE * PL::T, (TILE * PL::T <= 256) ? 2 : 1) k
         k0 += (((beta * RL) / Sp) % Rp) * mul;
         mul *= Rp;
       });
-      cplx cur = (STAGE != ST_C && a.twiddle) ? tw4step(a, (long long)n2 * k0)
-                                              : make_double2(1.0, 0.0);
+      cplx cur = (TW_A && a.twiddle) ? tw4step(a, (long long)n2 * k0)
+                                     : make_double2(1.0, 0.0);
 #pragma unroll
       for (int j = 0; j < RL; ++j) {
         const int k = k0 + j * (L1 / RL);
         cplx x = v[i * RL + j];
-        if (STAGE != ST_C && a.twiddle) {
+        if (TW_A && a.twiddle) {
           x = INV ? cmulc(x, cur) : cmul(x, cur);
           cur = cmul(cur, tws);
         }
@@ -184,16 +194,62 @@ __global__ void __launch_bounds__(TILE * PL::T, (TILE * PL::T <= 256) ? 2 : 1) k
     }
     __syncthreads();
     // coalesced tile store
-    for (int idx = threadIdx.x; idx < TILE * L1; idx += NT) {
-      const int cc = idx % TILE, n1 = idx / TILE, m2 = c0 + cc;
-      bool ok;
-      if (a.out.len >= 0)
-        ok = m2 < a.L2 && (long long)m2 + (long long)a.L2 * n1 < a.out.len;
-      else
-        ok = n1 < a.out.e1 && m2 < a.out.e2;
-      if (ok)
-        static_cast<cplx *>(a.out.ptr)[item * a.out.item_stride + n1 * a.out.s1 +
-                                       m2 * a.out.s2] = tile[cc * CS + n1];
+    auto store_tile = [&](const Out2 &o) {
+      for (int idx = threadIdx.x; idx < TILE * L1; idx += NT) {
+        const int cc = idx % TILE, n1 = idx / TILE, m2 = c0 + cc;
+        bool ok;
+        if (o.len >= 0)
+          ok = m2 < a.L2 && (long long)m2 + (long long)a.L2 * n1 < o.len;
+        else
+          ok = n1 < o.e1 && m2 < o.e2;
+        if (ok)
+          static_cast<cplx *>(o.ptr)[item * o.item_stride + n1 * o.s1 + m2 * o.s2] =
+              tile[cc * CS + n1];
+      }
+    };
+    if constexpr (PAIR) {
+      // col[k] = Z(k) = H(k) + i X(k) with H, X the column DFTs of the real
+      // h, x:  H(k) = (Z(k) + conj Z(-k)) / 2,  X(k) = (Z(k) - conj Z(-k)) / 2i,
+      // H(-k) = conj H(k), X(-k) = conj X(k).  Stage A of h is the INVERSE
+      // column DFT (= conj H for real h) times 1/L; both get the four-step
+      // twiddle W_L^{+-n2 k}.  Thread t handles the pairs (k, L1 - k),
+      // k = t, t + T, ... <= L1/2; x's values wait in registers while h's
+      // tile is stored.
+      // The pairs are disjoint and each is read and rewritten by one thread,
+      // so h's values go back in place at once.
+      constexpr int NP = (L1 / 2 + 1 + T - 1) / T;
+      cplx xa[NP], xb[NP];
+      const double sh = a.in.scale;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        const int k = t + p * T;
+        if (k > L1 / 2) continue;
+        const int kk = k == 0 ? 0 : L1 - k;
+        const cplx A = col[k], B = col[kk];
+        const cplx H = make_double2(0.5 * (A.x + B.x), 0.5 * (A.y - B.y));
+        const cplx X = make_double2(0.5 * (A.y + B.y), 0.5 * (B.x - A.x));
+        const cplx wk = tw4step(a, (long long)n2 * k), wkk = tw4step(a, (long long)n2 * kk);
+        // inverse h: conj(H(k)) * conj(W^{n2 k}) = conj(H(k) W^{n2 k})
+        const cplx hk = cmul(H, wk), hkk = cmulc(H, wkk);  // H(-k) = conj H(k)
+        xa[p] = cmul(X, wk);
+        xb[p] = cmul(make_double2(X.x, -X.y), wkk);
+        col[k] = make_double2(hk.x * sh, -hk.y * sh);
+        if (kk != k) col[kk] = make_double2(hkk.x * sh, hkk.y * sh);
+      }
+      __syncthreads();
+      store_tile(a.out);
+      __syncthreads();
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        const int k = t + p * T;
+        if (k > L1 / 2) continue;
+        col[k] = xa[p];
+        if (k != 0 && 2 * k != L1) col[L1 - k] = xb[p];  // kk == k for k = 0, L1/2
+      }
+      __syncthreads();
+      store_tile(a.out2);
+    } else {
+      store_tile(a.out);
     }
     __syncthreads();  // this buffer is refilled two iterations later
   }
@@ -294,6 +350,7 @@ bool supported_col_len(long long L1) {
 cudaError_t launch_cols(int stage, const large::ColArgs &a, long long items, int ncols,
                         cudaStream_t stream) {
   switch (stage) {
+    case large::ST_A_PAIR: return large::launch_cols_stage<large::ST_A_PAIR>(a, items, ncols, stream);
     case large::ST_A_FWD: return large::launch_cols_stage<large::ST_A_FWD>(a, items, ncols, stream);
     case large::ST_A_INV: return large::launch_cols_stage<large::ST_A_INV>(a, items, ncols, stream);
     default: return large::launch_cols_stage<large::ST_C>(a, items, ncols, stream);

@@ -7,7 +7,10 @@
 namespace hk {
 namespace large {
 
-enum ColStage : int { ST_A_FWD = 0, ST_A_INV = 1, ST_C = 2 };
+// ST_A_PAIR: real h (in) and real x (in2) packed as z = h + i x, ONE forward
+// column DFT, split by conjugate symmetry into the stage-A outputs of h
+// (inverse, scaled, -> out) and of x (forward, -> out2).
+enum ColStage : int { ST_A_FWD = 0, ST_A_INV = 1, ST_C = 2, ST_A_PAIR = 3 };
 
 // An operand viewed as an L1 x L2 array; element (n1, n2) of item b sits at
 // ptr + b*item_stride + n1*s1 + n2*s2 (elements).  Valid iff
@@ -34,6 +37,8 @@ struct Out2 {
 struct ColArgs {
   Op2 in;
   Out2 out;
+  Op2 in2;    // ST_A_PAIR only: the real vector x
+  Out2 out2;  // ST_A_PAIR only: stage-A output of x
   int32_t L1, L2;
   int32_t twiddle;       // 1: four-step twiddle W_L^{n2 k1} (1D mode); 0: 2D mode
   int32_t in_n1_fast;    // tile-load order: 1 when the operand is contiguous along n1

@@ -112,3 +112,25 @@ def test_every_column_length(L1):
     y = batched.hankel_tvp_partial(dh, [dx], shape, fft_len=L)[0].cpu().numpy()
     ref = O.hankel_tvp_partial(h, shape, [x])
     assert strict_relerr(y, ref) <= TOL
+
+
+@pytest.mark.parametrize("L1", [8, 12, 48, 96, 192, 384, 768, 1536])
+def test_real_pair_column_pass(L1):
+    """Real h with ONE real vector takes the packed z = h + i x column pass
+    (ST_A_PAIR): partial and full products, batch 2, forced column length."""
+    rng = np.random.default_rng(100 + L1)
+    L = L1 * 4096
+    n = L // 3                       # order 3: d_H = 3n - 2 <= L, two-level (> 8192)
+    shape = (n, n, n)
+    B = 2
+    h = rng.standard_normal((B, 3 * n - 2))
+    x = rng.uniform(-1.0, 1.0, (B, n))
+    dh = torch.from_numpy(h).cuda()
+    dx = torch.from_numpy(x).cuda()
+    y = batched.hankel_tvp_partial(dh, [dx, dx], shape, fft_len=L).cpu().numpy()
+    a = batched.hankel_tvp_full(dh, [dx, dx, dx], shape, fft_len=L).cpu().numpy()
+    for b in range(B):
+        ref = O.hankel_tvp_partial(h[b], shape, [x[b], x[b]])
+        assert strict_relerr(y[b], ref) <= TOL
+        a_ref = O.hankel_tvp_full(h[b], shape, [x[b]] * 3)
+        assert abs(a[b] - a_ref) <= TOL * abs(a_ref)
