@@ -22,7 +22,7 @@ HK_F64 = 1
 HK_SPEC = 2
 
 LIB_NAME = "libhankelfft_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("HK_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 
 class Operand(ctypes.Structure):
