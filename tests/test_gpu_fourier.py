@@ -46,3 +46,18 @@ def test_fft2_fftn():
     T = rng.standard_normal((5, 6, 7)) + 1j * rng.standard_normal((5, 6, 7))
     assert np.linalg.norm(P.fftn(T) - np.fft.fftn(T)) <= 1e-12 * np.linalg.norm(np.fft.fftn(T))
     assert np.linalg.norm(P.ifftn(T) - np.fft.ifftn(T)) <= 1e-12 * np.linalg.norm(np.fft.ifftn(T))
+
+
+def test_block_spectra_match_numpy():
+    """BhhbTensor / BaabTensor / LevelKHankelTensor .spectrum = ifft2 / ifftn of
+    the generator (block.py:65-69, 125-127, 214-216)."""
+    rng = np.random.default_rng(21)
+    H = rng.standard_normal((9, 7)) + 1j * rng.standard_normal((9, 7))
+    B = P.BhhbTensor(3, (3, 4, 4), (2, 3, 4), H)
+    np.testing.assert_allclose(B.spectrum, np.fft.ifft2(H), rtol=0, atol=1e-13)
+    C = rng.standard_normal((5, 6)) + 1j * rng.standard_normal((5, 6))
+    np.testing.assert_allclose(P.BaabTensor(3, C).spectrum, np.fft.ifft2(C), rtol=0, atol=1e-13)
+    levels = ((2, 3, 2), (3, 2, 2), (2, 2, 3))
+    G = rng.standard_normal((5, 5, 5)) + 1j * rng.standard_normal((5, 5, 5))
+    T = P.LevelKHankelTensor(3, levels, G)
+    np.testing.assert_allclose(T.spectrum, np.fft.ifftn(G), rtol=0, atol=1e-13)
