@@ -67,6 +67,7 @@ template <class PL, int G_>
 struct Regroup : PL {
   static constexpr int G = G_;
   static constexpr int CTA = G_ * PL::T;
+  static constexpr int kStagedBlocks = G_ >= 8 ? 3 : 24 / G_;  // resident CTAs with staging
   static constexpr int SMEM_BYTES = G_ * PL::L * (int)sizeof(cplx);
   static_assert(CTA % 32 == 0, "whole warps");
 };
@@ -82,9 +83,18 @@ struct Stage {
   static constexpr int BYTES = (SH + SX) * PL::CTA * (int)sizeof(cplx);
 };
 
+template <class T, class = void>
+struct requires_staged_blocks : std::false_type {};
+template <class T>
+struct requires_staged_blocks<T, std::void_t<decltype(T::kStagedBlocks)>> : std::true_type {};
+
 template <class PL, bool STG>
 constexpr int min_blocks_for() {
-  return STG ? 3 : Traits<PL>::min_blocks;
+  if constexpr (STG) {
+    if constexpr (requires_staged_blocks<PL>::value) return PL::kStagedBlocks;
+    return 3;
+  }
+  return Traits<PL>::min_blocks;
 }
 
 // STG: the next item's pass-0 operands (h and the first vector factor, raw
