@@ -361,8 +361,14 @@ int hk_plan_create_hankel(hk_plan **plan, int order, const int64_t *mode_sizes, 
         // smallest L; on ties prefer rows with a fast kernel, then fewer columns
         const bool fast2 = hk::fast_first_radix(l2) > 0;
         const bool bfast = best1 && hk::fast_first_radix(best2) > 0;
+        // HK_ROW_LEN: A/B knob preferring a row length among equal-L splits
+        // (B200 cfg3: 1536 x 8192 877 us, 2048 x 6144 1087 us)
+        static const long long want2 = getenv("HK_ROW_LEN") ? atoll(getenv("HK_ROW_LEN")) : 0;
+        const bool pref = want2 > 0 && l2 == want2, bpref = want2 > 0 && best2 == want2;
         if (!best1 || l < best1 * best2 ||
-            (l == best1 * best2 && (fast2 > bfast || (fast2 == bfast && l1 < best1)))) {
+            (l == best1 * best2 &&
+             (pref > bpref ||
+              (pref == bpref && (fast2 > bfast || (fast2 == bfast && l1 < best1)))))) {
           best1 = l1;
           best2 = l2;
         }

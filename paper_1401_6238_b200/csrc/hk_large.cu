@@ -17,6 +17,7 @@
 // columns that carry no data (x's zero block, unused outputs) are skipped.
 #include <atomic>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -321,7 +322,7 @@ static cudaError_t launch_cols_stage(const ColArgs &a, long long items, int ncol
     HK_COL(64, 32, Plan1D<64, 4, 4, 16>)
     HK_COL(96, 32, Plan1D<96, 6, 6, 16>)
     HK_COL(128, 16, Plan1D<128, 8, 8, 16>)
-    HK_COL(192, 16, Plan1D<192, 12, 12, 16>)
+    HK_COL(192, 8, Plan1D<192, 12, 12, 16>)  // B200 cfg4: TILE 8 973 us, 16 984, 32 1058
     HK_COL(256, 8, Plan1D<256, 16, 16, 16>)
     HK_COL(384, 8, Plan1D<384, 24, 24, 16>)
     HK_COL(512, 4, Plan1D<512, 32, 2, 16, 16>)
