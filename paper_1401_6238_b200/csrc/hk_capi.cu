@@ -602,6 +602,13 @@ int tl_run(const hk_plan *p, const hk_operand &h, const hk_operand *xs, int nx, 
   // column pass z = h + i x serves both (ST_A_PAIR).
   const bool pair = p->twiddle && what != 2 && h.dtype == HK_F64 && fs.size() == 1 &&
                     fs[0].op.dtype == HK_F64 && !getenv("HK_NO_PAIR");
+  // Real h and real vectors make the spectral product Hermitian,
+  // P(L - k) = conj P(k): rows k1 and L1 - k1 of every stage carry the same
+  // information (Q(L1-k1, m2) = conj(W_L2^{m2} Q(k1, m2))), so the row stage
+  // runs rows 0..L1/2 only and the final column pass synthesises the rest.
+  const bool half = pair && what == 0 && L1 % 2 == 0 && !getenv("HK_NO_HALF");
+  const long long rows_b = half ? L1 / 2 + 1 : L1;
+  ca.half = 0;
   for (long long b0 = 0; b0 < batch; b0 += chunk) {
     const long long nb = std::min(chunk, batch - b0);
     cudaError_t e;
@@ -620,8 +627,10 @@ int tl_run(const hk_plan *p, const hk_operand &h, const hk_operand *xs, int nx, 
       ca.in.len = d;
       ca.in_n1_fast = 0;
       ca.in2 = tl_vector_op(p, fs[0].op, fs[0].mode, b0, &pair_xcols);
-      ca.out = hk::large::Out2{Wh, L, L2, 1, -1, (int32_t)L1, (int32_t)L2};
-      ca.out2 = hk::large::Out2{Wx, L, L2, 1, -1, (int32_t)L1, (int32_t)L2};
+      // Hermitian product: rows k1 > L1/2 are never read (see `half` below)
+      const int32_t rows_out = half ? (int32_t)(L1 / 2 + 1) : (int32_t)L1;
+      ca.out = hk::large::Out2{Wh, L, L2, 1, -1, rows_out, (int32_t)L2};
+      ca.out2 = hk::large::Out2{Wx, L, L2, 1, -1, rows_out, (int32_t)L2};
       if ((e = hk::launch_cols(hk::large::ST_A_PAIR, ca, nb, hcols, st)) != cudaSuccess)
         return cuda_fail(e, "column stage (h + i x)");
     } else if (h.dtype == HK_SPEC) {
@@ -654,8 +663,8 @@ int tl_run(const hk_plan *p, const hk_operand &h, const hk_operand *xs, int nx, 
     }
     // ---- stage A: distinct vectors (forward)
     Args1D a{};
-    a.batch = nb * L1;
-    a.nsub = L1;
+    a.batch = nb * rows_b;
+    a.nsub = rows_b;
     a.tw = p->rtw;
     a.tw0 = p->rtw0;
     a.scale = 1.0;
@@ -733,6 +742,7 @@ int tl_run(const hk_plan *p, const hk_operand &h, const hk_operand *xs, int nx, 
         yout.e2 = (int32_t)p->inner[0];
       }
       ca.out = yout;
+      ca.half = half ? 1 : 0;
       if ((e = hk::launch_cols(hk::large::ST_C, ca, nb, ocols, st)) != cudaSuccess)
         return cuda_fail(e, "column stage (y)");
     } else {

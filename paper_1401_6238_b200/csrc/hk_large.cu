@@ -80,7 +80,9 @@ __global__ void __launch_bounds__(TILE * PL::T, (TILE * PL::T <= 256) ? 2 : 1) k
     const int c0 = (int)(w - item * tiles_per_item) * TILE;
     for (int idx = threadIdx.x; idx < TILE * L1; idx += NT) {
       const int cc = a.in_n1_fast ? idx / L1 : idx % TILE;
-      const int n1 = a.in_n1_fast ? idx - (idx / L1) * L1 : idx / TILE;
+      const int n1d = a.in_n1_fast ? idx - (idx / L1) * L1 : idx / TILE;
+      // Hermitian half (ST_C): rows above L1/2 are read from row L1 - n1
+      const int n1 = (STAGE == ST_C && a.half && 2 * n1d > L1) ? L1 - n1d : n1d;
       const int n2 = c0 + cc;
       bool ok;
       if (a.in.len >= 0)
@@ -88,7 +90,7 @@ __global__ void __launch_bounds__(TILE * PL::T, (TILE * PL::T <= 256) ? 2 : 1) k
       else
         ok = n1 < a.in.e1 && n2 < a.in.e2;
       const long long off = ok ? item * a.in.item_stride + n1 * a.in.s1 + n2 * a.in.s2 : 0;
-      const uint32_t dst = smem_u32(tile + cc * CS + fast::swz2(n1));
+      const uint32_t dst = smem_u32(tile + cc * CS + fast::swz2(n1d));
       if constexpr (PAIR) {  // z = h + i x from two real streams (1D layout)
         const bool ok2 = n2 < a.L2 && (long long)n2 + (long long)a.L2 * n1 < a.in2.len;
         const long long off2 =
@@ -133,9 +135,15 @@ __global__ void __launch_bounds__(TILE * PL::T, (TILE * PL::T <= 256) ? 2 : 1) k
     constexpr int S0 = PL::stride(0);
     cplx tw_cur = make_double2(1.0, 0.0), tw_step = make_double2(1.0, 0.0);
     if (STAGE == ST_C && a.twiddle) tw_step = tw4step(a, (long long)n2 * S0);
+    const cplx wrow = (STAGE == ST_C && a.half) ? tw4step(a, (long long)n2 * L1)
+                                                  : make_double2(1.0, 0.0);  // W_L2^{m2}
     auto in_load = [&](int, int j, int pos) {
       cplx v = col[fast::swz2(pos)];
       if constexpr (PAIR) return v;  // scale of h applied when z is split
+      if (STAGE == ST_C && a.half && 2 * pos > L1) {
+        v = cmul(v, wrow);  // Q(L1-k1, m2) = conj(W_L2^{m2} Q(k1, m2))
+        v.y = -v.y;
+      }
       if (real_in) v.y = 0.0;
       v.x *= a.in.scale;
       v.y *= a.in.scale;

@@ -47,6 +47,10 @@ struct ColArgs {
   const double2 *tlo;    // W_L^{r}, r < 4096
   const double2 *ctw;    // column plan table W_L1^e
   const double2 *ctw0;   // column plan first-pass table
+  // ST_C of a Hermitian spectral product (real h and x, 1D four-step): only
+  // rows k1 <= L1/2 of the row-stage output exist; row L1-k1 is synthesised
+  // as conj(W_L2^{m2} Q(k1, m2)) on load.
+  int32_t half;
 };
 
 }  // namespace large
