@@ -1,3 +1,4 @@
+# Development helper (run from the repo root: python tools/cfg4len.py ...); not part of the package or the tests.
 import sys, numpy as np, torch
 sys.path.insert(0, '.')
 from paper_1401_6238_b200 import batched, workloads

@@ -1,3 +1,4 @@
+# Development helper (run from the repo root: python tools/configs.py ...); not part of the package or the tests.
 import sys, time, numpy as np, torch
 sys.path.insert(0, '.')
 import paper_1401_6238_b200 as P

@@ -1,3 +1,4 @@
+# Development helper (run from the repo root: python tools/hooi.py ...); not part of the package or the tests.
 import sys, time, numpy as np, torch
 sys.path.insert(0, '.')
 from paper_1401_6238_b200 import batched, workloads

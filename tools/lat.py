@@ -1,3 +1,4 @@
+# Development helper (run from the repo root: python tools/lat.py ...); not part of the package or the tests.
 # Where does the numpy-facing latency of HankelTensor.tvp_partial go (cfg1)?
 import sys, time, ctypes, numpy as np, torch
 sys.path.insert(0, '.')

@@ -1,3 +1,4 @@
+# Development helper (run from the repo root: python tools/lencheck.py ...); not part of the package or the tests.
 import sys, numpy as np, torch
 sys.path.insert(0, '.')
 from oracle import hankel_oracle as O

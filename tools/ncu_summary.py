@@ -1,3 +1,4 @@
+# Development helper (run from the repo root: python tools/ncu_summary.py ...); not part of the package or the tests.
 import csv, subprocess, sys
 rep = sys.argv[1]
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
