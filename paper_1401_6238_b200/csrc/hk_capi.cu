@@ -816,13 +816,29 @@ int hk_tvp_partial_host(const hk_plan *plan, hk_operand h, const void *host_in, 
     if (x_offsets[i] < 0 || x_offsets[i] + plan->sizes[i + 1] > in_elems)
       return fail(HK_EINVAL, "vector %d lies outside the input buffer", i);
   cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n1 = plan->sizes[0];
+  hk_operand xs[hk::kMaxFactors];
+  // Zero-copy for the latency kernel's sizes: when both pinned buffers are
+  // mapped into the device address space (always, under UVA) the kernel reads
+  // the vectors and writes y over PCIe directly -- no copy launches.
+  void *din = nullptr, *dy = nullptr;
+  static const bool no_zc = getenv("HK_NO_ZEROCOPY") != nullptr;
+  if (!no_zc && plan->L[0] <= 4096 &&
+      cudaHostGetDevicePointer(&din, const_cast<void *>(host_in), 0) == cudaSuccess &&
+      cudaHostGetDevicePointer(&dy, host_y, 0) == cudaSuccess) {
+    for (int i = 0; i < nx; ++i)
+      xs[i] = hk_operand{static_cast<double2 *>(din) + x_offsets[i], 0, HK_C128, 0};
+    if ((rc = hk_tvp_partial(plan, h, xs, nx, 1, dy, n1, nullptr, stream))) return rc;
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    return HK_OK;
+  }
+  cudaGetLastError();  // clear a failed cudaHostGetDevicePointer
   cudaError_t e = cudaMemcpyAsync(dev_in, host_in, (size_t)in_elems * sizeof(double2),
                                   cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(H2D)");
-  hk_operand xs[hk::kMaxFactors];
   for (int i = 0; i < nx; ++i)
     xs[i] = hk_operand{static_cast<double2 *>(dev_in) + x_offsets[i], 0, HK_C128, 0};
-  const int64_t n1 = plan->sizes[0];
   if ((rc = hk_tvp_partial(plan, h, xs, nx, 1, dev_y, n1, nullptr, stream))) return rc;
   e = cudaMemcpyAsync(host_y, dev_y, (size_t)n1 * sizeof(double2), cudaMemcpyDeviceToHost, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(D2H)");
