@@ -81,6 +81,10 @@ class _Staging:
             self.host = torch.empty(cap, dtype=torch.complex128, pin_memory=True)
             self.devbuf = torch.empty(cap, dtype=torch.complex128, device=f"cuda:{self.dev}")
             self.cap = cap
+            # cached views / addresses for the latency path
+            self.hnp = self.host.numpy()
+            self.hbase = self.host.data_ptr()
+            self.dbase = self.devbuf.data_ptr()
         return self.host, self.devbuf
 
 
@@ -152,8 +156,8 @@ class HankelDeviceCache:
         st = _Staging.get(dev)
         n_in = sum(a.shape[0] for a in uniq)
         n1 = self.shape[0]
-        host, devbuf = st.ensure(n_in + n1)
-        hnp = host.numpy()
+        st.ensure(n_in + n1)
+        hnp = st.hnp
         offs, off = [], 0
         for a in uniq:
             hnp[off:off + a.shape[0]] = a
@@ -163,7 +167,7 @@ class HankelDeviceCache:
         plan = batched.hankel_plan(self.shape, dev)
         xoff = (ctypes.c_int64 * len(idx))(*[offs[i] for i in idx])
         hop = N.Operand(spec.data_ptr(), spec.stride(0), hkind, 0)
-        dbase, hbase = devbuf.data_ptr(), host.data_ptr()
+        dbase, hbase = st.dbase, st.hbase
         # one C call: H2D of the packed vectors, the product, D2H of y, sync
         N.check(N.load_library().hk_tvp_partial_host(
             plan.handle, hop, hbase, n_in, xoff, len(idx), dbase, dbase + 16 * n_in,
