@@ -61,8 +61,20 @@ __device__ __forceinline__ void cp_async_wait() {
 // Persistent column-tile kernel.  Tile w = (item, column block); the CTA keeps
 // two smem tile buffers and streams tile w+grid in with cp.async (zero-fill
 // for padding) while it transforms tile w, so global latency overlaps math.
+// Resident CTAs per SM the double-buffered tiles allow (227 KB of shared
+// memory); the register budget is sized so registers never cut below that.
+template <class PL, int TILE>
+constexpr int col_blocks() {
+  constexpr int pad = TILE >= 8 ? 1 : 8 / TILE;
+  constexpr int bytes = 2 * TILE * (PL::L + pad) * 16 + 1024;
+  constexpr int by_smem = (227 * 1024) / bytes;
+  constexpr int by_thr = 2048 / (TILE * PL::T);
+  constexpr int n = by_smem < by_thr ? by_smem : by_thr;
+  return n < 1 ? 1 : (n > 4 ? 4 : n);
+}
+
 template <class PL, int TILE, int STAGE>
-__global__ void __launch_bounds__(TILE * PL::T, (TILE * PL::T <= 256) ? 2 : 1) k_cols(const __grid_constant__ ColArgs a,
+__global__ void __launch_bounds__(TILE * PL::T, (col_blocks<PL, TILE>())) k_cols(const __grid_constant__ ColArgs a,
                                                           int tiles_per_item, long long ntiles) {
   constexpr int L1 = PL::L, T = PL::T, V = PL::V, RL = PL::Rlast, R0 = PL::radix[0];
   constexpr int PAD = TILE >= 8 ? 1 : 8 / TILE;
