@@ -162,6 +162,11 @@ __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const T
   constexpr bool HIM = Tr::hi_major(p);
   constexpr int NIN = FINAL ? R : NZ;
   constexpr int NOUT = FINAL ? NO : R;
+  // Pass-0 recurrence bases of a thread's NB butterflies, beta = t + i*T:
+  // W_L^beta = W_L^t * W_L^{i T}, the second factor a compile-time constant,
+  // so one table read serves all NB butterflies (8192 = 2 x 16^3: NB = 8).
+  [[maybe_unused]] cplx base0 = make_double2(1.0, 0.0);
+  if constexpr (p == 0 && PL::P > 1 && NB > 1 && std::is_same_v<TW0, Tw0Rec>) base0 = tw0.base(t);
 #pragma unroll
   for (int i = 0; i < NB; ++i) {
     const int beta = t + i * PL::T;
@@ -191,7 +196,16 @@ __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const T
       }
       auto twiddle = [&]() {
         if constexpr (p == 0 && PL::P > 1 && std::is_same_v<TW0, Tw0Rec>) {
-          twiddle_rec<R, INV>(a, tw0.base(beta));
+          if constexpr (NB > 1) {
+            cplx bi = base0;
+            sfor<NB>([&](auto ic) {  // constant index: bi = base0 * W_L^{i T}
+              constexpr int ii = decltype(ic)::value;
+              if (ii == i) bi = twc<ii * PL::T, PL::L, false>(base0);
+            });
+            twiddle_rec<R, INV>(a, bi);
+          } else {
+            twiddle_rec<R, INV>(a, tw0.base(beta));
+          }
         } else if constexpr (p == 0 && PL::P > 1) {
           // chunks of CK twiddles (j = CK*c+1 .. CK*c+CK) keep register pressure flat
           constexpr int CK = ChunkOf<TW0>::value;
