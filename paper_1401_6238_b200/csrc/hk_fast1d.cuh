@@ -1,7 +1,7 @@
 // K1/K2 fast path (kernel template; instantiated per FFT length in
-// hk_fast_*.cu so the lengths compile in parallel): fused batched 1D Hankel products with a TMEM-resident
-// spectral accumulator, pruned first/last passes and conflict-free,
-// low-traffic twiddle access.
+// hk_fast_*.cu so the lengths compile in parallel): fused batched 1D Hankel
+// products with a TMEM-resident spectral accumulator, pruned first/last
+// passes and conflict-free, low-traffic twiddle access.
 //
 // Per product (reference hankel.py:140-154 via hankel.py:42-71):
 //   acc  = ifft(h~)                        -> TMEM
@@ -13,13 +13,15 @@
 //   full:    alpha = sum(acc)              (fixed-order reduction)
 //
 // Differences from the generic kernel (hk_1d.cu):
-//  * acc lives in TMEM, so only one length-L working set is in registers:
-//    <= 128 registers/thread -> 2 CTAs (16 warps) per SM;
-//  * pass-0 twiddles come from a thread-major table (one coalesced 16 B load
-//    per value instead of a stride-j gather), middle passes map lanes onto the
-//    butterfly-group index so their twiddles are warp-uniform (broadcast);
+//  * acc lives in TMEM, so only one length-L working set is in registers;
+//  * twiddles: one table read per butterfly (pass 0: one per thread, the NB
+//    butterflies' bases follow by constant factors), the R-1 powers by a
+//    two-chain recurrence (fast::twiddle_rec) -- measured faster on B200 than
+//    the earlier thread-major pass-0 table and per-twiddle reads;
 //  * the smem swizzle XORs the low 3 position bits with bits 4-6 ^ 8-10, which
-//    keeps every 8-lane phase of every pass on distinct 16 B bank groups.
+//    keeps every 8-lane phase of every pass on distinct 16 B bank groups;
+//  * optional cp.async staging of the next item's pass-0 operands (STG) and
+//    regrouping of small products into multi-product CTAs (Regroup).
 #pragma once
 
 #include <atomic>
