@@ -1,0 +1,67 @@
+"""Randomised parity sweep over every dispatch path (latency kernel, ping-pong,
+fast, generic, two-level with packed/Hermitian real passes, block) against the
+CPU oracle: seeded shapes, orders, dtypes, batch sizes and repeated vectors."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import hankel_oracle as O
+from paper_1401_6238_b200 import batched
+from tests.helpers import strict_relerr
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def _vec(rng, shape, real):
+    v = rng.standard_normal(shape)
+    return v if real else v + 1j * rng.standard_normal(shape)
+
+
+CASES = []
+_rng = np.random.default_rng(2024)
+for k in range(120):
+    m = int(_rng.integers(2, 5))
+    scale = [40, 400, 1400, 5000, 30000][k % 5]
+    shape = tuple(int(_rng.integers(1, scale) + 1) for _ in range(m))
+    if k % 3 == 0:  # H x^{m-1}: equal trailing modes, one repeated vector
+        shape = (shape[0],) + (shape[1],) * (m - 1)
+    if sum(shape) - m + 1 > 200_000:
+        shape = tuple(max(1, n // 4) for n in shape)
+    B = int(_rng.choice([1, 2, 5, 40, 200])) if sum(shape) < 20000 else int(_rng.choice([1, 2]))
+    real = bool(_rng.integers(0, 2))
+    same = bool(_rng.integers(0, 2))
+    CASES.append((k, shape, B, real, same))
+
+
+@pytest.mark.parametrize("k,shape,B,real,same", CASES)
+def test_random_products(k, shape, B, real, same):
+    rng = np.random.default_rng(1000 + k)
+    m = len(shape)
+    d = sum(shape) - m + 1
+    h = _vec(rng, (B, d), real)
+    if same and len(set(shape[1:])) == 1:
+        x = _vec(rng, (B, shape[1]), real)
+        xs_np = [x] * (m - 1)
+        dx = torch.from_numpy(x).cuda()
+        xs = [dx] * (m - 1)
+    else:
+        xs_np = [_vec(rng, (B, n), real) for n in shape[1:]]
+        xs = [torch.from_numpy(x).cuda() for x in xs_np]
+    y = batched.hankel_tvp_partial(torch.from_numpy(h).cuda(), xs, shape).cpu().numpy()
+    for b in range(min(B, 3)):
+        ref = O.hankel_tvp_partial(h[b], shape, [x[b] for x in xs_np])
+        assert strict_relerr(y[b], ref) <= TOL, (k, shape, B, b)
+    # full product with one more vector of mode-1 length
+    x1 = _vec(rng, (B, shape[0]), real)
+    a = batched.hankel_tvp_full(torch.from_numpy(h).cuda(), [torch.from_numpy(x1).cuda()] + xs,
+                                shape).cpu().numpy()
+    for b in range(min(B, 3)):
+        a_ref = O.hankel_tvp_full(h[b], shape, [x1[b]] + [x[b] for x in xs_np])
+        # alpha = x1 . (H x_2 .. x_m): bound the error by |x1| |y| (a sum that
+        # cancels is not an error of the product)
+        y_ref = O.hankel_tvp_partial(h[b], shape, [x[b] for x in xs_np])
+        scale = np.linalg.norm(x1[b]) * np.linalg.norm(y_ref)
+        assert abs(a[b] - a_ref) <= TOL * scale, (k, shape, B, b)
