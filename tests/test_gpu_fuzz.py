@@ -65,3 +65,43 @@ def test_random_products(k, shape, B, real, same):
         y_ref = O.hankel_tvp_partial(h[b], shape, [x[b] for x in xs_np])
         scale = np.linalg.norm(x1[b]) * np.linalg.norm(y_ref)
         assert abs(a[b] - a_ref) <= TOL * scale, (k, shape, B, b)
+
+
+BLOCK_CASES = []
+_rng2 = np.random.default_rng(77)
+for k in range(30):
+    m = int(_rng2.integers(2, 4))
+    top = [12, 40, 90][k % 3]
+    block = tuple(int(_rng2.integers(1, top) + 1) for _ in range(m))
+    outer = tuple(int(_rng2.integers(1, top) + 1) for _ in range(m))
+    if k % 2 == 0:  # repeated vector
+        block = (block[0],) + (block[1],) * (m - 1)
+        outer = (outer[0],) + (outer[1],) * (m - 1)
+    B = int(_rng2.choice([1, 3, 17]))
+    BLOCK_CASES.append((k, block, outer, B))
+
+
+@pytest.mark.parametrize("k,block,outer,B", BLOCK_CASES)
+def test_random_block_products(k, block, outer, B):
+    rng = np.random.default_rng(5000 + k)
+    m = len(block)
+    din, dout = sum(block) - m + 1, sum(outer) - m + 1
+    H = rng.standard_normal((B, din, dout)) + 1j * rng.standard_normal((B, din, dout))
+    same = k % 2 == 0
+    xs_np = []
+    for p in range(1, m):
+        if same and p > 1:
+            xs_np.append(xs_np[0])
+        else:
+            n = block[p] * outer[p]
+            xs_np.append(rng.standard_normal((B, n)) + 1j * rng.standard_normal((B, n)))
+    dH = torch.from_numpy(H).cuda()
+    dxs, seen = [], {}
+    for x in xs_np:
+        if id(x) not in seen:
+            seen[id(x)] = torch.from_numpy(x).cuda()
+        dxs.append(seen[id(x)])
+    y = batched.bhhb_tvp_partial(dH, dxs, m, block, outer).cpu().numpy()
+    for b in range(min(B, 3)):
+        ref = O.bhhb_tvp_partial(H[b], block, outer, [x[b] for x in xs_np])
+        assert strict_relerr(y[b], ref) <= TOL, (k, block, outer, B, b)
