@@ -105,3 +105,35 @@ def test_random_block_products(k, block, outer, B):
     for b in range(min(B, 3)):
         ref = O.bhhb_tvp_partial(H[b], block, outer, [x[b] for x in xs_np])
         assert strict_relerr(y[b], ref) <= TOL, (k, block, outer, B, b)
+
+
+TM_CASES = []
+_rng3 = np.random.default_rng(99)
+for k in range(16):
+    m = int(_rng3.integers(2, 4))
+    n = int(_rng3.integers(2, 600))
+    shape = (int(_rng3.integers(2, 600)),) + (n,) * (m - 1)
+    r = int(_rng3.integers(1, 6))
+    TM_CASES.append((k, shape, r, int(_rng3.choice([1, 3]))))
+
+
+@pytest.mark.parametrize("k,shape,r,B", TM_CASES)
+def test_random_times_matrices(k, shape, r, B):
+    """times_matrices (hankel.py:174-194) with the same matrix for every mode
+    (symmetric dedupe + mirrored stores) and with distinct matrices."""
+    rng = np.random.default_rng(9000 + k)
+    m = len(shape)
+    d = sum(shape) - m + 1
+    h = rng.standard_normal((B, d)) + 1j * rng.standard_normal((B, d))
+    U = rng.standard_normal((B, shape[1], r)) + 1j * rng.standard_normal((B, shape[1], r))
+    dU = torch.from_numpy(U).cuda()
+    T = batched.times_matrices(torch.from_numpy(h).cuda(), shape, [dU] * (m - 1)).cpu().numpy()
+    mats = [rng.standard_normal((B, shape[1], r)) + 1j * rng.standard_normal((B, shape[1], r))
+            for _ in range(m - 1)]
+    T2 = batched.times_matrices(torch.from_numpy(h).cuda(), shape,
+                                [torch.from_numpy(M).cuda() for M in mats]).cpu().numpy()
+    for b in range(B):
+        ref = O.times_matrices(h[b], shape, [U[b]] * (m - 1))
+        assert strict_relerr(T[b], ref) <= TOL, (k, shape, r, b)
+        ref2 = O.times_matrices(h[b], shape, [M[b] for M in mats])
+        assert strict_relerr(T2[b], ref2) <= TOL, (k, shape, r, b)
