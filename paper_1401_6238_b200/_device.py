@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes
 import itertools
+import threading
 
 import numpy as np
 import torch
@@ -61,18 +62,25 @@ class _Staging:
     """
 
     _by_dev: dict = {}
+    _by_dev_lock = threading.Lock()
 
     def __init__(self, dev):
         self.dev = dev
         self.cap = 0
         self.host = None
         self.devbuf = None
+        # held from packing the inputs until the call's stream sync: the
+        # buffers are shared by every numpy-facing call on this device
+        self.lock = threading.RLock()
 
     @classmethod
     def get(cls, dev):
         st = cls._by_dev.get(dev)
         if st is None:
-            st = cls._by_dev[dev] = cls(dev)
+            with cls._by_dev_lock:
+                st = cls._by_dev.get(dev)
+                if st is None:
+                    st = cls._by_dev[dev] = cls(dev)
         return st
 
     def ensure(self, n):
@@ -146,14 +154,19 @@ class HankelDeviceCache:
             if plan.fft_lens[0] <= self.SMALL_L:
                 return self._lean_partial(dev, dh, uniq, idx, N.HK_C128)
             return self._lean_partial(dev, spec, uniq, idx)
-        up = _upload_packed(uniq, dev)
-        y = batched.hankel_tvp_partial(spec, [up[i] for i in idx], self.shape, spectrum=True)
-        return _download(y[0])
+        with _Staging.get(dev).lock:
+            up = _upload_packed(uniq, dev)
+            y = batched.hankel_tvp_partial(spec, [up[i] for i in idx], self.shape, spectrum=True)
+            return _download(y[0])
 
     def _lean_partial(self, dev, spec, uniq, idx, hkind=N.HK_SPEC) -> np.ndarray:
         """Latency path: one packed pinned H2D copy, a direct C-ABI call with
         cached plan/operand structs, one pinned D2H copy, one stream sync."""
         st = _Staging.get(dev)
+        with st.lock:
+            return self._lean_locked(st, dev, spec, uniq, idx, hkind)
+
+    def _lean_locked(self, st, dev, spec, uniq, idx, hkind) -> np.ndarray:
         n_in = sum(a.shape[0] for a in uniq)
         n1 = self.shape[0]
         st.ensure(n_in + n1)
@@ -177,13 +190,15 @@ class HankelDeviceCache:
     def tvp_full(self, xs) -> complex:
         dev, (dh, spec) = self._state()
         uniq, idx = _dedupe(xs)
-        up = _upload_packed(uniq, dev)
         plan = batched.hankel_plan(self.shape, dev)
-        if plan.workspace_per_item == 0 and plan.fft_lens[0] <= self.SMALL_L:
-            a = batched.hankel_tvp_full(dh, [up[i] for i in idx], self.shape)
-        else:
-            a = batched.hankel_tvp_full(spec, [up[i] for i in idx], self.shape, spectrum=True)
-        return complex(_download(a)[0])
+        with _Staging.get(dev).lock:
+            up = _upload_packed(uniq, dev)
+            if plan.workspace_per_item == 0 and plan.fft_lens[0] <= self.SMALL_L:
+                a = batched.hankel_tvp_full(dh, [up[i] for i in idx], self.shape)
+            else:
+                a = batched.hankel_tvp_full(spec, [up[i] for i in idx], self.shape,
+                                            spectrum=True)
+            return complex(_download(a)[0])
 
     def times_matrices(self, mats) -> np.ndarray:
         dev, spec = self._spec()

@@ -252,3 +252,31 @@ def test_lazy_conj_views_are_materialised():
                                    shape).cpu().numpy()
     ref = np.stack([O.hankel_tvp_partial(h[b], shape, [np.conj(x[b]), z[b]]) for b in range(2)])
     assert strict_relerr(y, ref) <= TOL
+
+
+def test_concurrent_numpy_calls_are_independent():
+    """Several host threads share the per-device staging buffers of the
+    numpy-facing path; every call must still return its own product
+    (reference SPEC: deterministic results regardless of schedule)."""
+    import threading
+
+    rng = np.random.default_rng(31)
+    cases = []
+    for k in range(8):
+        shape = (100 + k, 120, 120)
+        h = rand_vec(rng, sum(shape) - 2)
+        x = rand_vec(rng, 120)
+        cases.append((P.HankelTensor(shape, h), x, O.hankel_tvp_partial(h, shape, [x, x])))
+    errs = []
+
+    def work(T, x, ref):
+        for _ in range(20):
+            y = T.tvp_partial([x, x])
+            errs.append(strict_relerr(y, ref))
+
+    ths = [threading.Thread(target=work, args=c) for c in cases]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert len(errs) == 160 and max(errs) <= 1e-12
