@@ -226,6 +226,23 @@ class BhhbDeviceCache:
             self._per_dev[dev] = dH
         return dev, dH
 
+    def native_supported(self) -> bool:
+        """True when the native 2D block plan covers this generator."""
+        dev = require_cuda()
+        try:
+            batched.bhhb_plan(self.order, self.block_shape, self.outer_shape, dev)
+        except NotImplementedError:
+            return False
+        return True
+
+    def times_matrices(self, mats) -> np.ndarray:
+        dev, dH = self._H()
+        uniq, idx = _dedupe(mats)
+        up = _upload(uniq, dev)
+        T = batched.bhhb_times_matrices(dH, [up[i] for i in idx], self.order, self.block_shape,
+                                        self.outer_shape)
+        return T[0].cpu().numpy()
+
     def tvp_partial(self, xs) -> np.ndarray:
         dev, dH = self._H()
         uniq, idx = _dedupe(xs)

@@ -14,6 +14,7 @@ Shapes (B = batch of independent tensors):
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import torch
 
@@ -192,6 +193,49 @@ def hankel_tvp_full(h: torch.Tensor, xs, shape, *, spectrum: bool = False,
     return alpha
 
 
+def _times_matrices_plan(plan, h, mats, sizes, n1, spectrum, what):
+    """hk_times_matrices on an existing plan; mats[p] (B, sizes[p], R_p)."""
+    mats = _physical_list(mats)
+    h = _physical(h)
+    dev = _dev_index(h)
+    B = h.shape[0]
+    for p, M in enumerate(mats):
+        _require_cuda(M, f"mats[{p}]")
+        if M.dim() != 3 or M.shape[1] != sizes[p] or M.dtype != torch.complex128:
+            raise ValueError(f"matrix {p} must be (B, {sizes[p]}, R) complex128")
+        if M.stride(2) != 1 or M.stride(1) != M.shape[2]:
+            raise ValueError(f"matrix {p} must be row-major contiguous per item")
+    ranks = [int(M.shape[2]) for M in mats]
+    lib = N.load_library()
+    r_arr = N.i64_array(ranks)
+    ws_bytes = lib.hk_times_matrices_workspace_bytes(plan.handle, r_arr, len(mats), B)
+    ws = torch.empty((max(int(ws_bytes), 16),), dtype=torch.uint8, device=h.device)
+    T = torch.empty((B, n1, *ranks), dtype=torch.complex128, device=h.device)
+    ptrs = (ctypes.c_void_p * len(mats))(*[M.data_ptr() for M in mats])
+    strides = N.i64_array([M.stride(0) for M in mats])
+    N.check(lib.hk_times_matrices(plan.handle, _operand(h, "h", spectrum), ptrs, strides,
+                                  r_arr, len(mats), B, T.data_ptr(),
+                                  T[0].numel() if B else 0, ws.data_ptr(), _stream(dev)), what)
+    return T
+
+
+def bhhb_times_matrices(H: torch.Tensor, mats, order, block_shape, outer_shape) -> torch.Tensor:
+    """Batched BHHB T_b[:, j_2..j_m] = H_b x_2 M_2[:, j_2] ... (hankel.py:174-194 over
+    block.py:136-144).  H: (B, d_in, d_out); mats[p]: (B, n_{p+2} N_{p+2}, R_p)
+    whose rows are column-stacked (F-order) block vectors.  Returns
+    (B, n_1 N_1, R_2, ..., R_m) complex128 (two-level 2D plans only)."""
+    block_shape, outer_shape = tuple(block_shape), tuple(outer_shape)
+    if len(mats) != order - 1:
+        raise ValueError(f"expected {order - 1} matrices, got {len(mats)}")
+    dev = _dev_index(H)
+    with _OnDevice(dev):
+        plan = bhhb_plan(order, block_shape, outer_shape, dev)
+        Hf = _physical(H).reshape(H.shape[0], -1)
+        sizes = [block_shape[p] * outer_shape[p] for p in range(1, order)]
+        return _times_matrices_plan(plan, Hf, mats, sizes, block_shape[0] * outer_shape[0],
+                                    False, "hk_times_matrices(block)")
+
+
 def times_matrices(h: torch.Tensor, shape, mats, *, spectrum: bool = False,
                    fft_len: int = 0) -> torch.Tensor:
     """T_b[:, j_2..j_m] = H_b x_2 M_2[:, j_2] ... (reference hankel.py:174-194).
@@ -202,33 +246,13 @@ def times_matrices(h: torch.Tensor, shape, mats, *, spectrum: bool = False,
     """
     shape = tuple(int(n) for n in shape)
     m = len(shape)
-    mats = _physical_list(mats)
-    h = _physical(h)
     if len(mats) != m - 1:
         raise ValueError(f"expected {m - 1} matrices, got {len(mats)}")
     dev = _dev_index(h)
-    B = h.shape[0]
-    for p, M in enumerate(mats):
-        _require_cuda(M, f"mats[{p}]")
-        if M.dim() != 3 or M.shape[1] != shape[p + 1] or M.dtype != torch.complex128:
-            raise ValueError(f"matrix {p} must be (B, {shape[p + 1]}, R) complex128")
-        if M.stride(2) != 1 or M.stride(1) != M.shape[2]:
-            raise ValueError(f"matrix {p} must be row-major contiguous per item")
-    ranks = [int(M.shape[2]) for M in mats]
     with _OnDevice(dev):
         plan = hankel_plan(shape, dev, fft_len)
-        lib = N.load_library()
-        r_arr = N.i64_array(ranks)
-        ws_bytes = lib.hk_times_matrices_workspace_bytes(plan.handle, r_arr, len(mats), B)
-        ws = torch.empty((max(int(ws_bytes), 16),), dtype=torch.uint8, device=h.device)
-        T = torch.empty((B, shape[0], *ranks), dtype=torch.complex128, device=h.device)
-        ptrs = (ctypes.c_void_p * len(mats))(*[M.data_ptr() for M in mats])
-        strides = N.i64_array([M.stride(0) for M in mats])
-        N.check(lib.hk_times_matrices(plan.handle, _operand(h, "h", spectrum), ptrs, strides,
-                                      r_arr, len(mats), B, T.data_ptr(),
-                                      T[0].numel() if B else 0, ws.data_ptr(), _stream(dev)),
-                "hk_times_matrices")
-    return T
+        return _times_matrices_plan(plan, h, mats, shape[1:], shape[0], spectrum,
+                                    "hk_times_matrices")
 
 
 def _block_operand(t: torch.Tensor, name: str, length: int, spectrum: bool = False):
@@ -308,9 +332,15 @@ def bhhb_tvp_full(H: torch.Tensor, xs, order, block_shape, outer_shape) -> torch
 
 
 class _HostPipeline:
-    """Per-(device, shape) double-buffered device staging for host-buffer calls."""
+    """Per-(device, shape) double-buffered device staging for host-buffer calls.
+
+    ``lock`` is held while one call enqueues its chunks: the staging buffers
+    and streams are shared by every host thread using this key, and the
+    stream order then keeps one call's copies and kernels from touching
+    another's buffers."""
 
     def __init__(self, dev, d, ns, n1, chunk, real_h, real_x):
+        self.lock = threading.Lock()
         self.streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
         hd = torch.float64 if real_h else torch.complex128
         xd = torch.float64 if real_x else torch.complex128
@@ -323,6 +353,7 @@ class _HostPipeline:
 
 
 _pipelines: dict = {}
+_pipelines_lock = threading.Lock()
 
 
 def hankel_tvp_partial_host(h: torch.Tensor, xs, shape, *, out: torch.Tensor | None = None,
@@ -355,25 +386,27 @@ def hankel_tvp_partial_host(h: torch.Tensor, xs, shape, *, out: torch.Tensor | N
     real_h = h.dtype == torch.float64
     real_x = all(u.dtype == torch.float64 for u in uniq)
     key = (dev, shape, int(h.shape[1]), tuple(ns), chunk, real_h, real_x)
-    pipe = _pipelines.get(key)
-    if pipe is None:
-        pipe = _HostPipeline(dev, int(h.shape[1]), ns, shape[0], chunk, real_h, real_x)
-        _pipelines[key] = pipe
+    with _pipelines_lock:
+        pipe = _pipelines.get(key)
+        if pipe is None:
+            pipe = _HostPipeline(dev, int(h.shape[1]), ns, shape[0], chunk, real_h, real_x)
+            _pipelines[key] = pipe
     if out is None:
         out = torch.empty((B, shape[0]), dtype=torch.complex128, pin_memory=True)
     cur = torch.cuda.current_stream(dev)
-    for s in pipe.streams:
-        s.wait_stream(cur)
-    for c, start in enumerate(range(0, B, chunk)):
-        nb = min(chunk, B - start)
-        st, buf = pipe.streams[c % 2], pipe.bufs[c % 2]
-        with torch.cuda.stream(st):
-            buf["h"][:nb].copy_(h[start:start + nb], non_blocking=True)
-            for k, u in enumerate(uniq):
-                buf["xs"][k][:nb].copy_(u[start:start + nb], non_blocking=True)
-            hankel_tvp_partial(buf["h"][:nb], [buf["xs"][i][:nb] for i in idx], shape,
-                               out=buf["y"][:nb])
-            out[start:start + nb].copy_(buf["y"][:nb], non_blocking=True)
-    for s in pipe.streams:
-        cur.wait_stream(s)
+    with pipe.lock:
+        for s in pipe.streams:
+            s.wait_stream(cur)
+        for c, start in enumerate(range(0, B, chunk)):
+            nb = min(chunk, B - start)
+            st, buf = pipe.streams[c % 2], pipe.bufs[c % 2]
+            with torch.cuda.stream(st):
+                buf["h"][:nb].copy_(h[start:start + nb], non_blocking=True)
+                for k, u in enumerate(uniq):
+                    buf["xs"][k][:nb].copy_(u[start:start + nb], non_blocking=True)
+                hankel_tvp_partial(buf["h"][:nb], [buf["xs"][i][:nb] for i in idx], shape,
+                                   out=buf["y"][:nb])
+                out[start:start + nb].copy_(buf["y"][:nb], non_blocking=True)
+        for s in pipe.streams:
+            cur.wait_stream(s)
     return out

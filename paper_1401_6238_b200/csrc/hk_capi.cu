@@ -440,6 +440,10 @@ int hk_plan_create_block(hk_plan **plan, int order, int levels, const int64_t *l
         break;
       }
   }
+  const bool auto2 = !(fft_lens && fft_lens[0] > 0), auto1 = !(fft_lens && fft_lens[1] > 0);
+  if ((auto2 && L2 <= 0) || (auto1 && L1 <= 0))  // no supported length covers the generator
+    return fail(HK_EUNSUPPORTED, "block generator %lldx%lld exceeds the supported lengths", din,
+                dout);
   if (L2 < din || L1 < dout) return fail(HK_EINVAL, "fft lengths shorter than the generator");
   if (L2 <= 0 || !hk::supported_1d(L2) || !hk::supported_col_len(L1))
     return fail(HK_EUNSUPPORTED, "block generator %lldx%lld exceeds the supported lengths", din,
@@ -515,8 +519,10 @@ int launch_row(long long L2, const Args1D &a, cudaStream_t st) {
 int elem_bytes(int32_t dtype) { return dtype == HK_F64 ? 8 : 16; }
 
 // Operand of mode `mode` (0-based) of a two-level plan as an L1 x L2 array.
+// `es` is the element stride inside one vector (1 = contiguous; a column of a
+// row-major matrix with R columns has es = R).
 hk::large::Op2 tl_vector_op(const hk_plan *p, const hk_operand &o, int mode, long long b0,
-                            int *ncols) {
+                            int *ncols, long long es = 1) {
   hk::large::Op2 op{};
   op.ptr = static_cast<const char *>(o.data) + b0 * o.batch_stride * elem_bytes(o.dtype);
   op.item_stride = o.batch_stride;
@@ -524,14 +530,14 @@ hk::large::Op2 tl_vector_op(const hk_plan *p, const hk_operand &o, int mode, lon
   op.scale = 1.0;
   if (p->twiddle) {  // 1D four-step
     const long long n = p->sizes[mode];
-    op.s1 = p->L2;
-    op.s2 = 1;
+    op.s1 = p->L2 * es;
+    op.s2 = es;
     op.len = n;
     *ncols = (int)std::min<long long>(p->L2, n);
   } else {  // 2D block: F-order (inner n x outer N), element (i, j) at i + n j
     const long long n = p->inner[mode], N = p->outer[mode];
-    op.s1 = n;
-    op.s2 = 1;
+    op.s1 = n * es;
+    op.s2 = es;
     op.len = -1;
     op.e1 = (int32_t)N;
     op.e2 = (int32_t)n;
@@ -540,9 +546,11 @@ hk::large::Op2 tl_vector_op(const hk_plan *p, const hk_operand &o, int mode, lon
   return op;
 }
 
-// what: 0 partial (y), 1 full (alpha), 2 spectrum (stage-A output of h)
+// what: 0 partial (y), 1 full (alpha), 2 spectrum (stage-A output of h).
+// xes: per-vector element strides (NULL = contiguous); oes: element stride of y.
 int tl_run(const hk_plan *p, const hk_operand &h, const hk_operand *xs, int nx, int mode_offset,
-           int64_t batch, void *out, int64_t out_stride, void *ws, void *stream, int what) {
+           int64_t batch, void *out, int64_t out_stride, void *ws, void *stream, int what,
+           const long long *xes = nullptr, long long oes = 1) {
   if (batch == 0) return HK_OK;
   if (!ws) return fail(HK_EINVAL, "two-level plans need a workspace of hk_workspace_bytes()");
   cudaStream_t st = (cudaStream_t)stream;
@@ -552,6 +560,7 @@ int tl_run(const hk_plan *p, const hk_operand &h, const hk_operand *xs, int nx, 
     hk_operand op;
     int mode;
     int power;
+    long long es;
   };
   std::vector<Fac> fs;
   for (int i = 0; i < nx; ++i) {
@@ -559,16 +568,17 @@ int tl_run(const hk_plan *p, const hk_operand &h, const hk_operand *xs, int nx, 
     if (xs[i].dtype != HK_C128 && xs[i].dtype != HK_F64)
       return fail(HK_EINVAL, "vector %d: two-level plans take raw vectors", i);
     const int mode = i + mode_offset;
+    const long long es = xes ? xes[i] : 1;
     bool merged = false;
     for (auto &f : fs)
       if (f.op.data == xs[i].data && f.op.batch_stride == xs[i].batch_stride &&
-          f.op.dtype == xs[i].dtype && p->sizes[f.mode] == p->sizes[mode] &&
+          f.op.dtype == xs[i].dtype && f.es == es && p->sizes[f.mode] == p->sizes[mode] &&
           (p->twiddle || (p->inner[f.mode] == p->inner[mode]))) {
         ++f.power;
         merged = true;
         break;
       }
-    if (!merged) fs.push_back({xs[i], mode, 1});
+    if (!merged) fs.push_back({xs[i], mode, 1, es});
   }
   if ((int)fs.size() > p->order || (int)fs.size() > hk::kMaxFactors)
     return fail(HK_EUNSUPPORTED, "too many distinct vectors for the two-level workspace");
@@ -626,7 +636,7 @@ int tl_run(const hk_plan *p, const hk_operand &h, const hk_operand *xs, int nx, 
       ca.in.s2 = 1;
       ca.in.len = d;
       ca.in_n1_fast = 0;
-      ca.in2 = tl_vector_op(p, fs[0].op, fs[0].mode, b0, &pair_xcols);
+      ca.in2 = tl_vector_op(p, fs[0].op, fs[0].mode, b0, &pair_xcols, fs[0].es);
       // Hermitian product: rows k1 > L1/2 are never read (see `half` below)
       const int32_t rows_out = half ? (int32_t)(L1 / 2 + 1) : (int32_t)L1;
       ca.out = hk::large::Out2{Wh, L, L2, 1, -1, rows_out, (int32_t)L2};
@@ -683,7 +693,7 @@ int tl_run(const hk_plan *p, const hk_operand &h, const hk_operand *xs, int nx, 
       if (pair) {
         ncols = pair_xcols;  // written by the packed pass above
       } else {
-        ca.in = tl_vector_op(p, fs[f].op, fs[f].mode, b0, &ncols);
+        ca.in = tl_vector_op(p, fs[f].op, fs[f].mode, b0, &ncols, fs[f].es);
         ca.in_n1_fast = 0;
         ca.out = hk::large::Out2{wx, L, L2, 1, -1, (int32_t)L1, (int32_t)ncols};
         if ((e = hk::launch_cols(hk::large::ST_A_FWD, ca, nb, ncols, st)) != cudaSuccess)
@@ -731,12 +741,12 @@ int tl_run(const hk_plan *p, const hk_operand &h, const hk_operand *xs, int nx, 
       yout.ptr = static_cast<double2 *>(out) + b0 * out_stride;
       yout.item_stride = out_stride;
       if (p->twiddle) {
-        yout.s1 = L2;
-        yout.s2 = 1;
+        yout.s1 = L2 * oes;
+        yout.s2 = oes;
         yout.len = p->sizes[0];
       } else {
-        yout.s1 = p->inner[0];
-        yout.s2 = 1;
+        yout.s1 = p->inner[0] * oes;
+        yout.s2 = oes;
         yout.len = -1;
         yout.e1 = (int32_t)p->outer[0];
         yout.e2 = (int32_t)p->inner[0];
@@ -749,6 +759,71 @@ int tl_run(const hk_plan *p, const hk_operand &h, const hk_operand *xs, int nx, 
       if ((e = hk::launch_rowsum(part, L1, static_cast<double2 *>(out) + b0, nb, st)) !=
           cudaSuccess)
         return cuda_fail(e, "row-sum kernel");
+    }
+  }
+  return HK_OK;
+}
+
+}  // namespace
+
+namespace {
+
+// times_matrices for two-level plans (L > 8192 1D four-step, 2D block): one
+// four-step product per column combination, the columns read in place from
+// the row-major matrices (element stride R) and T written in place (element
+// stride = number of combinations).  The spectrum of h is computed once.  When
+// m = 3 and both matrices are the same, only j2 <= j3 is computed and the
+// result mirrored to T[:, j3, j2] by a strided device copy.
+int tl_times_matrices(const hk_plan *p, const hk_operand &h, const void *const *mats,
+                      const int64_t *mat_strides, const int64_t *ranks, int nmats, int64_t batch,
+                      void *T, int64_t t_stride, void *workspace, void *stream,
+                      long long ncombo) {
+  const long long L = hk_plan_spectrum_len(p);
+  double2 *wsb = static_cast<double2 *>(workspace);
+  hk_operand hs = h;
+  int rc;
+  if (h.dtype != HK_SPEC) {
+    if ((rc = tl_run(p, h, nullptr, 0, 0, batch, wsb, 0, wsb + batch * L, stream, 2))) return rc;
+    hs = hk_operand{wsb, L, HK_SPEC, 0};
+    wsb += batch * L;
+  }
+  for (int i = 0; i < nmats; ++i)
+    if (!mats[i]) return fail(HK_EINVAL, "matrix %d pointer is NULL", i);
+  const bool sym2 = nmats == 2 && mats[0] == mats[1] && mat_strides[0] == mat_strides[1] &&
+                    ranks[0] == ranks[1] && p->sizes[1] == p->sizes[2];
+  const long long n1 = p->sizes[0];
+  std::vector<hk_operand> xs(nmats);
+  std::vector<long long> es(nmats), j(nmats);
+  for (long long c = 0; c < ncombo; ++c) {
+    long long rem = c;
+    for (int i = nmats - 1; i >= 0; --i) {
+      j[i] = rem % ranks[i];
+      rem /= ranks[i];
+    }
+    if (sym2 && j[1] < j[0]) continue;
+    for (int i = 0; i < nmats; ++i) {
+      xs[i] = hk_operand{static_cast<const double2 *>(mats[i]) + j[i], mat_strides[i], HK_C128, 0};
+      es[i] = ranks[i];
+    }
+    if ((rc = tl_run(p, hs, xs.data(), nmats, 1, batch, static_cast<double2 *>(T) + c, t_stride,
+                     wsb, stream, 0, es.data(), ncombo)))
+      return rc;
+    if (sym2 && j[1] != j[0]) {
+      const long long c2 = j[1] * ranks[1] + j[0];
+      const size_t pitch = (size_t)ncombo * sizeof(double2);
+      cudaStream_t st = (cudaStream_t)stream;
+      cudaError_t e = cudaSuccess;
+      if (t_stride == n1 * ncombo) {
+        e = cudaMemcpy2DAsync(static_cast<double2 *>(T) + c2, pitch, static_cast<double2 *>(T) + c,
+                              pitch, sizeof(double2), (size_t)(batch * n1),
+                              cudaMemcpyDeviceToDevice, st);
+      } else {
+        for (long long b = 0; b < batch && e == cudaSuccess; ++b)
+          e = cudaMemcpy2DAsync(static_cast<double2 *>(T) + b * t_stride + c2, pitch,
+                                static_cast<double2 *>(T) + b * t_stride + c, pitch,
+                                sizeof(double2), (size_t)n1, cudaMemcpyDeviceToDevice, st);
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "mirror copy of a symmetric combination");
     }
   }
   return HK_OK;
@@ -874,6 +949,10 @@ int hk_vector_spectra(const hk_plan *plan, int mode, const void *mats, int64_t m
   if (ncols < 1 || batch < 0) return fail(HK_EINVAL, "bad ncols/batch");
   if (batch == 0) return HK_OK;
   if (!mats || !spec) return fail(HK_EINVAL, "NULL matrix or spectrum pointer");
+  if (plan->two_level)
+    return fail(HK_EUNSUPPORTED,
+                "column spectra exist for on-chip plans only (two-level plans transform the "
+                "columns inside hk_times_matrices)");
   const long long L = plan->L[0];
   Args1D a = base_args(plan, batch * ncols);
   a.nsub = ncols;
@@ -896,6 +975,9 @@ int hk_vector_spectra(const hk_plan *plan, int mode, const void *mats, int64_t m
 size_t hk_times_matrices_workspace_bytes(const hk_plan *plan, const int64_t *ranks, int nmats,
                                          int64_t batch) {
   if (!plan || !ranks || batch <= 0) return 0;
+  if (plan->two_level)  // cached spectrum of h + the four-step workspace
+    return (size_t)batch * (size_t)hk_plan_spectrum_len(plan) * sizeof(double2) +
+           hk_workspace_bytes(plan, batch);
   long long cols = 1;  // spectrum of h
   for (int i = 0; i < nmats; ++i) cols += ranks[i];
   return (size_t)cols * (size_t)plan->L[0] * (size_t)batch * sizeof(double2);
@@ -917,6 +999,9 @@ int hk_times_matrices(const hk_plan *plan, hk_operand h, const void *const *mats
   }
   if (batch == 0) return HK_OK;
   if (!T || !workspace) return fail(HK_EINVAL, "NULL output or workspace");
+  if (plan->two_level)
+    return tl_times_matrices(plan, h, mats, mat_strides, ranks, nmats, batch, T, t_stride,
+                             workspace, stream, ncombo);
   const long long L = plan->L[0];
   double2 *ws = static_cast<double2 *>(workspace);
   long long used = 0;

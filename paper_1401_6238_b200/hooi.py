@@ -45,17 +45,39 @@ def leading_left_singular(M: torch.Tensor, r: int) -> torch.Tensor:
     G, U = M V Sigma^{-1}.  Leading singular vectors only depend on the
     leading part of the spectrum, so squaring the condition number costs
     ~eps*sigma_1^2/gap^2 (measured 2e-13 on cfg5 against the SVD) while the
-    batched library SVD of 256 x (2000 x 25) is ~500x slower.  Other shapes use
-    the SVD.
+    batched library SVD of 256 x (2000 x 25) is ~500x slower.  The shortcut is
+    only trusted when it is well posed: items whose r-th eigenvalue gap is
+    below 1e-5 sigma_1^2, whose r-th singular value vanishes, or whose factor
+    is not orthonormal to 1e-12 (rank-deficient or ill-conditioned M) are
+    recomputed with the SVD, which always returns orthonormal factors like
+    the reference.  Other shapes use the SVD directly.
     """
     rows, cols = M.shape[-2], M.shape[-1]
-    if rows >= 2 * cols and r <= cols:
-        G = M.conj().transpose(-1, -2) @ M
-        w, V = torch.linalg.eigh(G)
-        V = V[..., -r:].flip(-1)
-        s = torch.sqrt(torch.clamp(w[..., -r:].flip(-1), min=0.0))
+    if not 1 <= r <= min(rows, cols):
+        raise ValueError(f"rank {r} out of range for a {(rows, cols)} matrix")
+    if rows >= 2 * cols:
+        batch_shape = M.shape[:-2]
+        Mb = M.reshape(-1, rows, cols)
+        G = Mb.conj().transpose(-1, -2) @ Mb
+        w, V = torch.linalg.eigh(G)                       # ascending
+        Vr = V[..., -r:].flip(-1)
+        wr = w[..., -r:].flip(-1)
+        w1 = w[..., -1].clamp(min=torch.finfo(w.dtype).tiny)
+        w_next = w[..., -r - 1] if r < cols else torch.zeros_like(w1)
+        gap = (w[..., -r] - w_next) / w1
+        s = torch.sqrt(torch.clamp(wr, min=0.0))
+        ok = (s[..., -1] > 0) & (gap >= 1e-5)
         s = torch.where(s > 0, s, torch.ones_like(s))
-        return fix_phase_batched((M @ V.to(M.dtype)) / s[..., None, :].to(M.dtype))
+        U = (Mb @ Vr.to(Mb.dtype)) / s[..., None, :].to(Mb.dtype)
+        eye = torch.eye(r, dtype=U.dtype, device=U.device)
+        ortho = (U.conj().transpose(-1, -2) @ U - eye).abs().amax(dim=(-2, -1))
+        ok &= (ortho <= 1e-12) & torch.isfinite(ortho)
+        if not bool(ok.all()):
+            bad = torch.nonzero(~ok).flatten()
+            Us, _, _ = torch.linalg.svd(Mb[bad], full_matrices=False)
+            U = U.clone()
+            U[bad] = Us[..., :r]
+        return fix_phase_batched(U).reshape(*batch_shape, rows, r)
     U, _, _ = torch.linalg.svd(M, full_matrices=False)
     return fix_phase_batched(U[..., :r])
 
@@ -101,7 +123,17 @@ class TuckerResult:
 
 
 def hooi_symmetric(tensor, rank: int, tol: float = 1e-10, max_iter: int = 100) -> TuckerResult:
-    """decompose.py:142-184 for a square ``HankelTensor``, products on the GPU."""
+    """decompose.py:142-184 with the products and factor updates on the GPU.
+
+    Like the reference, ``tensor`` may be any square structured tensor exposing
+    ``mode_sizes``, ``tvp_partial`` and ``reduced_unfold_1`` (Hankel, BHHB,
+    level-k).  A ``HankelTensor`` keeps its spectrum and every T on the device
+    (fused ``hk_times_matrices``); other tensors go through their own
+    ``times_matrices`` (hankel.py:174-194 contract), with the factor updates
+    still batched on the device.
+    """
+    from .hankel import HankelTensor, times_matrices as tm_generic
+
     sizes = tensor.mode_sizes
     if len(set(sizes)) != 1:
         raise ValueError("symmetric HOOI requires equal mode sizes")
@@ -110,15 +142,25 @@ def hooi_symmetric(tensor, rank: int, tol: float = 1e-10, max_iter: int = 100) -
     if not 1 <= rank <= n:
         raise ValueError(f"rank {rank} out of range for size {n}")
     dev = require_cuda()
-    h = torch.from_numpy(np.ascontiguousarray(tensor.h)).to(f"cuda:{dev}")[None]
-    spec = batched.hankel_spectrum(h, sizes)
-    A = torch.from_numpy(np.ascontiguousarray(tensor.reduced_unfold_1())).to(h.device)[None]
-    U = leading_left_singular(A, rank)
+    device = f"cuda:{dev}"
+    A = torch.from_numpy(np.ascontiguousarray(tensor.reduced_unfold_1())).to(device)[None]
+    U = leading_left_singular(A.to(torch.complex128), rank)
+
+    if isinstance(tensor, HankelTensor):
+        h = torch.from_numpy(np.ascontiguousarray(tensor.h)).to(device)[None]
+        spec = batched.hankel_spectrum(h, sizes)
+
+        def products(Umat):
+            Uc = torch.conj_physical(Umat).contiguous()
+            return batched.times_matrices(spec, sizes, [Uc] * (m - 1), spectrum=True)[0]
+    else:
+        def products(Umat):
+            Uc = np.conj(Umat[0].cpu().numpy())
+            return torch.from_numpy(tm_generic(tensor, [Uc] * (m - 1))).to(device)
 
     def core_with(Umat):
-        Uc = torch.conj_physical(Umat).contiguous()
-        T = batched.times_matrices(spec, sizes, [Uc] * (m - 1), spectrum=True)
-        S = torch.tensordot(T[0], Umat[0].conj(), dims=([0], [0]))
+        T = products(Umat)
+        S = torch.tensordot(T, Umat[0].conj(), dims=([0], [0]))
         return T, torch.movedim(S, -1, 0)
 
     T, S = core_with(U)

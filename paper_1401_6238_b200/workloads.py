@@ -81,3 +81,20 @@ def _fix_phase(U):
     a = U[idx, np.arange(U.shape[1])]
     scale = np.where(np.abs(a) > 0, np.conj(a) / np.where(np.abs(a) > 0, np.abs(a), 1), 1)
     return U * scale[None, :]
+
+
+def tm_large_inputs():
+    """Seeded inputs of the two-level times_matrices parity cases
+    (oracle/gen_golden_r2.py, tests/test_gpu_tm_large.py): order 3 with n = 3000
+    (d_H = 8998) and r = 3, and order 2 (5000, 4000) with r = 2."""
+    rng = np.random.default_rng(777)
+
+    def rv(n):
+        return rng.standard_normal(n) + 1j * rng.standard_normal(n)
+
+    h3 = rv(8998)
+    M3 = rv(3000 * 3).reshape(3000, 3)
+    M3b = rv(3000 * 3).reshape(3000, 3)
+    h2 = rv(8999)
+    M2 = rv(4000 * 2).reshape(4000, 2)
+    return h3, M3, M3b, h2, M2
