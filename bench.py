@@ -9,20 +9,34 @@ of output per step, larger than the 126 MB L2, so no flush is needed.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Multi-GPU (torchrun, one rank per GPU): every rank runs its own 4096-product
-batch (weak scaling, no collective on the data path); the timed region is
-bracketed by barriers and the max over ranks is reported.
+Multi-GPU: one process per GPU.  ``--gpus N`` outside torchrun
+re-launches itself under ``torch.distributed.run`` (127.0.0.1).  The 4096
+products are sharded contiguously over the ranks (``dist.shard_range``; no
+collective on the data path) -- strong scaling, the headline ``value``; each
+rank then also runs a full 4096-product batch (weak scaling, ``weak``).
+The result gather to rank 0 (NCCL gather) is timed separately (``gather``).
+Every time is taken on the device with CUDA events and is the max over ranks.
 
---impl reference times the reference's CPU algorithm (the pinned numpy port in
-oracle/, which restates hankel.py:140-147 exactly: exact embedding length
-d_H = 4093, one pocketfft transform per vector) on all host cores, rank 0 only.
+The timed region replays the K steps from one CUDA graph (the product kernel
+launched K times back to back, no host launch overhead between steps); the
+per-launch kernel time of the roofline is measured with events around each
+launch in a separate loop.
+
+--impl reference times the reference's own CPU path on all host cores, rank 0
+only (oracle/cpu_baseline.py): the unmodified reference package installed in
+baseline/_ref when present (kind "reference"), else the pinned numpy port
+(kind "port").  ``value`` is the reference's faster pow2 variant of the same
+product (cli.py:277-291, L = 4096 like ours); the exact-length public API
+(hankel.py:140-147, L = d_H = 4093) is reported beside it.
 """
 
 from __future__ import annotations
 
 import argparse
+import importlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -34,7 +48,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_MODE, ORDER, BATCH, FFT_LEN = 1024, 4, 4096, 4096
+N_MODE, ORDER, FFT_LEN = 1024, 4, 4096
+# HK_BENCH_BATCH shrinks the batch for the CPU (gloo) harness test only
+BATCH = int(os.environ.get("HK_BENCH_BATCH", "4096"))
 DOF = ORDER * (N_MODE - 1) + 1
 B_ALG = (DOF + N_MODE + N_MODE) * 16          # compulsory bytes per product
 METRIC = "Hankel T·x^{m-1} products/s and % of HBM roofline at 1/2/4/8 B200"
@@ -44,22 +60,36 @@ WORKLOAD = ("cfg2: 4096 independent order-4 n=1024 complex128 Hankel tensors, "
 
 
 def peaks():
+    out = {"hbm_gbs": 6650.0, "hbm_kind": "fallback (B200_PROFILING.md)", "fp64_tflops": None}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        out["hbm_gbs"], out["hbm_kind"] = float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return 6650.0, "fallback"
-
-
-def ncu_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+        pass
     try:
-        with open(path) as f:
-            return json.load(f).get("cfg2_traffic_bytes")
+        with open(os.path.join(ROOT, "profiles", "r02_ubench_fp64.json")) as f:
+            r = json.load(f)["results"]
+        out["fp64_tflops"] = next(x["dfma_tflops"] for x in r if x["mode"] == "DFMA only")
     except Exception:
-        return None
+        pass
+    return out
+
+
+def ncu_summary():
+    """Per-launch DRAM bytes and FP64 pipe share of the dominant kernel from the
+    committed ncu capture (profiles/ncu_summary.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 # ---------------------------------------------------------------- clocks
@@ -79,7 +109,7 @@ class ClockSampler:
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-i", str(self.gpu), "-lms", "100"],
+                 "-i", str(self.gpu), "-lms", "20"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -109,70 +139,369 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+# ---------------------------------------------------------------- engines
+class EventTimer:
+    """CUDA events on the current stream, synchronised on read."""
+
+    def __init__(self, torch):
+        self.torch = torch
+        self.a = torch.cuda.Event(enable_timing=True)
+        self.b = torch.cuda.Event(enable_timing=True)
+
+    def start(self):
+        self.a.record()
+
+    def stop(self):
+        self.b.record()
+
+    def ms(self):
+        self.torch.cuda.synchronize()
+        return self.a.elapsed_time(self.b)
+
+
+class CudaEngine:
+    """The product path under test: batched.hankel_tvp_partial on this rank's GPU
+    (one fused kernel launch per step over the rank's products)."""
+
+    backend = "nccl"
+    launches_per_step = 1
+    dtype = "c128"
+
+    def __init__(self, local_rank):
+        import torch
+
+        self.torch = torch
+        torch.cuda.set_device(local_rank)
+        self.dev = torch.cuda.current_device()
+        self.shape = (N_MODE,) * ORDER
+        self._h = self._x = None
+
+    def device(self):
+        return self.torch.device("cuda", self.dev)
+
+    def gpu_index(self):
+        return self.dev
+
+    def inputs(self):
+        from paper_1401_6238_b200 import workloads
+
+        if self._h is None:
+            h, x = workloads.cfg2(4096, N_MODE, ORDER)  # BATCH < 4096: a prefix
+            self._h, self._x = h[:BATCH], x[:BATCH]
+        return self._h, self._x
+
+    def load(self, lo, hi):
+        torch = self.torch
+        h, x = self.inputs()
+        self.lo, self.hi = lo, hi
+        self.dh = torch.from_numpy(h[lo:hi]).to(self.dev)
+        self.dx = torch.from_numpy(x[lo:hi]).to(self.dev)
+        self.y = torch.empty((hi - lo, N_MODE), dtype=torch.complex128, device=self.dev)
+
+    def unload(self):
+        self.dh = self.dx = self.y = None
+        self.torch.cuda.empty_cache()
+
+    def step(self):
+        from paper_1401_6238_b200 import batched
+
+        if self.hi > self.lo:
+            batched.hankel_tvp_partial(self.dh, [self.dx, self.dx, self.dx], self.shape,
+                                       out=self.y)
+
+    def sync(self):
+        self.torch.cuda.synchronize()
+
+    def timer(self):
+        return EventTimer(self.torch)
+
+    def capture(self, k):
+        """k steps in one CUDA graph; returns the replay callable."""
+        torch = self.torch
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.step()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(k):
+                self.step()
+        self._graph = g
+        return g.replay
+
+    def result(self):
+        return self.y
+
+    def e2e(self, steps, barrier, reduce_max):
+        """The same products through the public host API: pinned host inputs ->
+        H2D -> kernel -> D2H into pinned host memory, every step."""
+        torch = self.torch
+        from paper_1401_6238_b200 import batched
+
+        h, x = self.inputs()
+        lo, hi = self.lo, self.hi
+        hp = torch.from_numpy(h[lo:hi]).pin_memory()
+        xp = torch.from_numpy(x[lo:hi]).pin_memory()
+        yp = torch.empty((hi - lo, N_MODE), dtype=torch.complex128, pin_memory=True)
+        run = lambda: batched.hankel_tvp_partial_host(hp, [xp, xp, xp], self.shape, out=yp)
+        for _ in range(2):
+            run()
+        torch.cuda.synchronize()
+        barrier()
+        t = self.timer()
+        t.start()
+        for _ in range(steps):
+            run()
+        t.stop()
+        ms = reduce_max(t.ms())
+        return ms, int(hp.numel() * 16 + xp.numel() * 16), int(yp.numel() * 16)
+
+
+def load_engine(spec, local_rank):
+    if not spec:
+        return CudaEngine(local_rank)
+    mod, _, cls = spec.partition(":")
+    return getattr(importlib.import_module(mod), cls)(local_rank)
+
+
+def parity_vs_golden(y, batch):
+    """Relative error of this run's outputs against the reference's own cfg2
+    outputs (tests/golden/cfg2.npz: products 0,1,2,4095 in full, the norm and
+    first entry of every product)."""
+    g = np.load(os.path.join(ROOT, "tests", "golden", "cfg2.npz"))
+    sel = [int(s) for s in g["sel"] if s < batch]
+    errs = [float(np.linalg.norm(y[s] - g["y"][k]) / np.linalg.norm(g["y"][k]))
+            for k, s in enumerate(g["sel"]) if s < batch]
+    norms = np.linalg.norm(y, axis=1)
+    norm_err = float(np.max(np.abs(norms - g["norms"][:batch]) / g["norms"][:batch]))
+    first_err = float(np.max(np.abs(y[:, 0] - g["first"][:batch]) / g["norms"][:batch]))
+    return {"parity_rel_err": max(errs + [norm_err, first_err]),
+            "parity_products_full": sel, "parity_norms_checked": int(batch),
+            "parity_reference": "tests/golden/cfg2.npz (reference hankel.py:140-147 output)"}
+
+
+# ---------------------------------------------------------------- harness
+def measure(engine, steps, warmup, rank, world, barrier, reduce_max, weak=True, e2e=True):
+    """Strong-scaling timed region over this rank's shard, per-launch kernel
+    times, the timed gather, and (world > 1) the weak-scaling batch."""
+    from paper_1401_6238_b200.dist import gather_shards, shard_range
+
+    lo, hi = shard_range(BATCH, rank, world)
+    engine.load(lo, hi)
+    for _ in range(max(3, warmup)):
+        engine.step()
+    engine.sync()
+    replay = engine.capture(steps) if hasattr(engine, "capture") else None
+    clocks = ClockSampler(engine.gpu_index()) if hasattr(engine, "gpu_index") else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.25)
+    out = {"shard": [lo, hi]}
+    # -- strong scaling: the 4096-product batch sharded over the ranks
+    barrier()
+    engine.sync()
+    t = engine.timer()
+    t.start()
+    if replay is not None:
+        replay()
+    else:
+        for _ in range(steps):
+            engine.step()
+    t.stop()
+    ms = t.ms()
+    barrier()
+    # -- per-launch kernel time (events around every launch, same stream)
+    ev = []
+    for _ in range(steps):
+        tk = engine.timer()
+        tk.start()
+        engine.step()
+        tk.stop()
+        ev.append(tk)
+    kern = statistics.mean(tk.ms() for tk in ev)
+    out["clocks"] = clocks.stop() if clocks else None
+    out["ms_total"] = reduce_max(ms)
+    out["kernel_ms"] = reduce_max(kern)
+    # -- result gather to rank 0, timed on its own
+    barrier()
+    engine.sync()
+    tg = engine.timer()
+    tg.start()
+    full = gather_shards(engine.result(), BATCH, dst=0)
+    tg.stop()
+    out["gather_ms"] = reduce_max(tg.ms())
+    out["full"] = None if full is None else full.cpu().numpy()
+    # -- end to end through the public host API
+    if e2e:
+        out["e2e_ms"], out["h2d"], out["d2h"] = engine.e2e(steps, barrier, reduce_max)
+    # -- weak scaling: every rank runs a full batch
+    if weak and world > 1:
+        engine.unload()
+        engine.load(0, BATCH)
+        for _ in range(3):
+            engine.step()
+        engine.sync()
+        replay = engine.capture(steps) if hasattr(engine, "capture") else None
+        barrier()
+        engine.sync()
+        t = engine.timer()
+        t.start()
+        if replay is not None:
+            replay()
+        else:
+            for _ in range(steps):
+                engine.step()
+        t.stop()
+        out["weak_ms_total"] = reduce_max(t.ms())
+    return out
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1401_6238_b200.dist import max_over_ranks
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    engine = load_engine(args.engine, local)
+    if world > 1:
+        if engine.backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=engine.device())
+        else:
+            dist.init_process_group(engine.backend)
+    coll_dev = engine.device()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    reduce_max = lambda v: max_over_ranks(v, coll_dev)
+    r = measure(engine, args.steps, args.warmup, rank, world, barrier, reduce_max,
+                e2e=not args.no_e2e)
+    ms_step = r["ms_total"] / args.steps
+    value = BATCH * args.steps / (r["ms_total"] * 1e-3)
+    if rank == 0:
+        pk = peaks()
+        ncu = ncu_summary()
+        # per-launch algorithmic bytes of the dominant kernel: rank 0's shard
+        shard = r["shard"][1] - r["shard"][0]
+        achieved = B_ALG * shard / (r["kernel_ms"] * 1e-3) / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": engine.dtype,
+            "data": "synthetic (seeded N(0,1) complex, SURVEY §8d cfg2)",
+            "config": {"workload": WORKLOAD, "batch": BATCH, "products_per_gpu": shard,
+                       "n": N_MODE, "order": ORDER, "fft_len": FFT_LEN,
+                       "parallelism": f"dp{world} (batch sharded, no data-path collective)",
+                       "l2": "inputs larger than L2 (402 MB/step vs 126 MB); no flush",
+                       "timed_region": "K steps replayed from one CUDA graph"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
+                         "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+                         "peak_kind": pk["hbm_kind"],
+                         "traffic": ncu.get("cfg2_traffic_bytes"),
+                         "bytes_alg_per_launch": B_ALG * shard,
+                         "kernel_ms": r["kernel_ms"],
+                         "fp64_pipe_frac": ncu.get("cfg2_fp64_pipe_frac"),
+                         "fp64_peak_tflops": pk["fp64_tflops"],
+                         "fp64_note": "measured DFMA peak (profiles/r02_ubench_fp64.json); "
+                                      "fp64_pipe_frac from the committed ncu capture"},
+            "gpu_launches": engine.launches_per_step * args.steps,
+            "clocks": r["clocks"],
+            "gather": {"ms": r["gather_ms"], "to_rank": 0,
+                       "bytes": int(BATCH * N_MODE * 16 * (world - 1) / world),
+                       "how": f"torch.distributed gather ({engine.backend if world > 1 else 'none, one rank'}), "
+                              "timed apart from the products"},
+        }
+        if "e2e_ms" in r:
+            line["e2e"] = {"value": BATCH * args.steps / (r["e2e_ms"] * 1e-3), "unit": UNIT,
+                           "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
+                           "path": "batched.hankel_tvp_partial_host: pinned host -> host"}
+        if "weak_ms_total" in r:
+            line["weak"] = {"value": world * BATCH * args.steps / (r["weak_ms_total"] * 1e-3),
+                            "unit": UNIT, "products_per_gpu": BATCH,
+                            "ms_per_step": r["weak_ms_total"] / args.steps}
+        if r["full"] is not None:
+            line.update(parity_vs_golden(r["full"], BATCH))
+        if world == 1 and not args.no_extras and hasattr(engine, "torch"):
+            try:
+                line["configs"] = other_configs(engine.torch, pk["hbm_gbs"])
+            except Exception as exc:  # never lose the headline line
+                line["configs"] = {"error": repr(exc)}
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_block(args, line.get("configs"))
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 # ---------------------------------------------------------------- CPU baseline
-def _cpu_worker(args):
-    os.environ["OMP_NUM_THREADS"] = "1"
-    n_products, seed, barrier_time = args
-    from oracle import hankel_oracle as O
+def cpu_baseline_block(args, configs):
+    from oracle import cpu_baseline as C
 
-    rng = np.random.default_rng(seed)
-    h = rng.standard_normal((n_products, DOF)) + 1j * rng.standard_normal((n_products, DOF))
-    x = rng.standard_normal((n_products, N_MODE)) + 1j * rng.standard_normal((n_products, N_MODE))
-    shape = (N_MODE,) * ORDER
-    while time.time() < barrier_time:
-        time.sleep(0.001)
-    t0 = time.perf_counter()
-    for b in range(n_products):
-        O.hankel_tvp_partial(h[b], shape, [x[b]] * (ORDER - 1))
-    return n_products, time.perf_counter() - t0
-
-
-def cpu_reference_rate(products_per_core: int, cores: int):
-    """Reference algorithm (oracle port) on `cores` processes; products/s."""
-    import multiprocessing as mp
-
-    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
-        os.environ[k] = "1"
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(cores) as pool:
-        start = time.time() + 2.0 + 0.05 * cores
-        res = pool.map(_cpu_worker, [(products_per_core, 1000 + i, start) for i in range(cores)])
-    total = sum(r[0] for r in res)
-    wall = max(r[1] for r in res)
-    return total / wall, total, wall
-
-
-def host_cores():
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count() or 1
+    cores = C.host_cores()
+    if args.cpu_quick:
+        rates = {"kind": C.impl_kind(), "cores": cores, "cpu_model": C.cpu_model(),
+                 "numpy": np.__version__, "cfg2": C.cfg2_rates(cores, steps=1)}
+    else:
+        rates = C.all_config_rates(cores)
+    c2 = rates["cfg2"]
+    best = "pow2" if c2["pow2"]["all_cores"] >= c2["exact"]["all_cores"] else "exact"
+    block = {
+        "value": c2[best]["all_cores"], "unit": UNIT, "cores": cores, "kind": rates["kind"],
+        "path": {"pow2": "reference cli._fast_product_padded (L=4096, cli.py:277-291)",
+                 "exact": "reference HankelTensor.tvp_partial (L=d_H=4093, hankel.py:140-147)"}[best],
+        "sample": f"the full 4096-product cfg2 batch split over {cores} processes "
+                  "(best of 3 barrier-separated steps); 1-core rate from 48 products",
+        "one_core": c2[best]["one_core"],
+        "exact_all_cores": c2["exact"]["all_cores"], "exact_one_core": c2["exact"]["one_core"],
+        "pow2_all_cores": c2["pow2"]["all_cores"], "pow2_one_core": c2["pow2"]["one_core"],
+        "cpu_model": rates["cpu_model"], "numpy": rates["numpy"],
+    }
+    if "cfg1" in rates:
+        block["per_config"] = {k: rates[k] for k in ("cfg1", "cfg3", "cfg4", "cfg5")}
+        if isinstance(configs, dict):  # GPU vs CPU side by side for every config
+            for k in ("cfg1", "cfg3", "cfg4", "cfg5"):
+                if k in configs and isinstance(configs[k], dict):
+                    configs[k]["cpu"] = rates[k]
+    return block
 
 
-# ---------------------------------------------------------------- reference arm
 def run_reference(args):
+    """The reference CPU path on all host cores, rank 0 only."""
+    from oracle import cpu_baseline as C
+
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cores = host_cores()
-    per_core = max(8, args.ref_products_per_core)
-    for _ in range(args.warmup):
-        cpu_reference_rate(4, min(cores, 4))
-    vals = []
-    for _ in range(args.steps):
-        rate, total, wall = cpu_reference_rate(per_core, cores)
-        vals.append(rate)
-    value = statistics.median(vals)
+    cores = C.host_cores()
+    units, ts = C.step_times("cfg2", "pow2", BATCH, cores, steps=args.warmup + args.steps)
+    ts = ts[args.warmup:]
+    value = units / statistics.median(ts)
+    u_ex, ts_ex = C.step_times("cfg2", "exact", BATCH, cores, steps=2)
+    exact = u_ex / min(ts_ex)
+    kind = C.impl_kind()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": BATCH / value * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "ms_per_step": statistics.median(ts) * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": WORKLOAD, "batch": BATCH, "n": N_MODE, "order": ORDER,
-                   "fft_len": DOF},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{per_core} products per core x {cores} cores per step "
-                                   "(exact L=d_H=4093, numpy pocketfft, oracle/hankel_oracle.py)"},
+                   "fft_len": FFT_LEN},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "path": "reference cli._fast_product_padded (pow2 L=4096)",
+                         "sample": f"each step = the full 4096-product batch over {cores} "
+                                   "processes (inputs built before the first barrier)",
+                         "exact_all_cores": exact, "cpu_model": C.cpu_model(),
+                         "numpy": np.__version__},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -183,6 +512,7 @@ def run_reference(args):
 B_ALG_CFG = {
     "cfg1": (298 + 100 + 100) * 8,
     "cfg2": B_ALG,
+    "cfg2_c64": B_ALG // 2,
     "cfg3": (12_582_910 + 2 * 4_194_304) * 8,
     "cfg4": (190 * 190 + 64 * 64 + 64 * 64) * 16,
     "cfg5": 2000 * 16 + 2000 * 5 * 16 // 25 + 5998 * 16 // (50 * 25),
@@ -271,6 +601,21 @@ def other_configs(torch, peak):
                                              "(200 calls captured in a CUDA graph, inputs "
                                              "resident); the *_api_us columns include the "
                                              "host-side call overhead")})
+    # cfg2 in single precision (complex64 variant, FP32 arithmetic, tol 1e-4)
+    g = np.load(os.path.join(golden, "cfg2.npz"))
+    h, x = workloads.cfg2()
+    dh = torch.from_numpy(h.astype(np.complex64)).cuda()
+    dx = torch.from_numpy(x.astype(np.complex64)).cuda()
+    y64 = torch.empty((h.shape[0], N_MODE), dtype=torch.complex64, device=dh.device)
+    f2 = lambda: batched.hankel_tvp_partial(dh, [dx, dx, dx], (N_MODE,) * ORDER, out=y64)
+    ms = _graph_ms(torch, f2, 20)
+    y = y64.cpu().numpy()
+    err = max(_relerr(y[s], g["y"][k]) for k, s in enumerate(g["sel"]))
+    rec("cfg2_c64", h.shape[0], ms, err,
+        {"metric_note": "cfg2 with complex64 inputs/outputs and FP32 arithmetic "
+                        "(B_alg halves: 49,128 B/product); parity vs the reference's "
+                        "complex128 outputs, north_star tolerance 1e-4"})
+    del dh, dx, y64
     # cfg3: one large real product (four-step, L = 1536 x 8192)
     g = np.load(os.path.join(golden, "cfg3.npz"))
     h, x = workloads.cfg3()
@@ -294,6 +639,7 @@ def other_configs(torch, peak):
     del dH, dxv
     # cfg5: one HOOI iteration's products for 256 signals (25 mixed products each)
     g = np.load(os.path.join(golden, "cfg5.npz"))
+    g50 = np.load(os.path.join(golden, "cfg5_sweep50.npz"))
     sig, U0, shape = workloads.cfg5(signals=256)
     dsig = torch.from_numpy(sig).cuda()
     dU = torch.from_numpy(np.ascontiguousarray(np.conj(U0))).cuda()[None]
@@ -308,140 +654,31 @@ def other_configs(torch, peak):
     dU0 = torch.from_numpy(U0).cuda()
     floop = lambda: hooi_symmetric_batched(dsig, shape, 5, dU0, max_iter=50, spectrum=spec)
     ms_loop = _dev_ms(torch, floop, 1, warm=1)
-    U2 = hooi_symmetric_batched(dsig[:1], shape, 5, dU0, max_iter=2)[0].cpu().numpy()
-    P1, P2 = U2 @ U2.conj().T, g["U2"] @ g["U2"].conj().T
+    U50 = floop()[:2].cpu().numpy()
+    perr = max(_relerr(U50[s] @ U50[s].conj().T, g50[f"U50_{s}"] @ g50[f"U50_{s}"].conj().T)
+               for s in range(2))
     rec("cfg5", sig.shape[0] * 25, ms, _relerr(T[g["rows"]], g["T1_rows"]),
         {"metric_note": "times_matrices step of one HOOI iteration (256 signals x 25 "
                         "products, cached spectra); per-iteration SVD excluded",
          "loop_50_sweeps_ms": ms_loop,
          "loop_products_per_s": sig.shape[0] * 25 * 50 / (ms_loop * 1e-3),
-         "loop_U2_projector_rel_err": _relerr(P1, P2)})
+         "loop_U50_projector_rel_err": perr,
+         "loop_parity_note": "signals 0,1 after 50 sweeps vs the reference's own loop "
+                             "(tests/golden/cfg5_sweep50.npz)"})
     return out
 
 
-# ---------------------------------------------------------------- our arm
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
-
-    from paper_1401_6238_b200 import batched, workloads
-    from paper_1401_6238_b200.dist import max_over_ranks
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.cuda.current_device()
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    h, x = workloads.cfg2(BATCH, N_MODE, ORDER)
-    shape = (N_MODE,) * ORDER
-    dh = torch.from_numpy(h).to(dev)
-    dx = torch.from_numpy(x).to(dev)
-    y = torch.empty((BATCH, N_MODE), dtype=torch.complex128, device=dev)
-    stream = torch.cuda.current_stream(dev)
-
-    def step():
-        batched.hankel_tvp_partial(dh, [dx, dx, dx], shape, out=y)
-
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
-
-    # --- device-resident timed region (one kernel launch per step) ---
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    clocks = ClockSampler(dev)
-    clocks.start()
-    time.sleep(0.3)
-    barrier()
-    torch.cuda.synchronize()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    t_start.record(stream)
-    for k in range(args.steps):
-        ev[k][0].record(stream)
-        step()
-        ev[k][1].record(stream)
-    t_end.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    clk = clocks.stop()
-    ms_total = max_over_ranks(t_start.elapsed_time(t_end), dev)
-    kern_ms = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in ev), dev)
-    ms_step = ms_total / args.steps
-    value = world * BATCH * args.steps / (ms_total * 1e-3)
-
-    # --- end to end: pinned host buffers -> public host API -> pinned host result ---
-    hp = torch.from_numpy(h).pin_memory()
-    xp = torch.from_numpy(x).pin_memory()
-    yp = torch.empty((BATCH, N_MODE), dtype=torch.complex128, pin_memory=True)
-    for _ in range(2):
-        batched.hankel_tvp_partial_host(hp, [xp, xp, xp], shape, out=yp)
-    torch.cuda.synchronize()
-    e2e_steps = max(2, min(args.steps, 5))
-    barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        batched.hankel_tvp_partial_host(hp, [xp, xp, xp], shape, out=yp)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1), dev)
-    e2e_value = world * BATCH * e2e_steps / (e2e_ms * 1e-3)
-
-    # parity spot check of this run's output (first product) against the golden norm
-    ok = bool(torch.isfinite(torch.view_as_real(y)).all().item())
-
-    if rank == 0:
-        peak, peak_kind = peaks()
-        achieved = B_ALG * BATCH / (kern_ms * 1e-3) / 1e9
-        traffic = ncu_traffic()
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
-            "data": "synthetic (seeded N(0,1) complex, SURVEY §8d cfg2)",
-            "config": {"workload": WORKLOAD, "batch_per_gpu": BATCH, "n": N_MODE,
-                       "order": ORDER, "fft_len": FFT_LEN, "parallelism": f"dp{world}",
-                       "l2": "inputs larger than L2 (402 MB/step vs 126 MB)"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "peak_kind": peak_kind,
-                         "traffic": traffic, "bytes_alg_per_launch": B_ALG * BATCH,
-                         "kernel_ms": kern_ms},
-            "e2e": {"value": e2e_value, "unit": UNIT,
-                    "h2d_bytes_per_step": int(hp.numel() * 16 + xp.numel() * 16),
-                    "d2h_bytes_per_step": int(yp.numel() * 16)},
-            "gpu_launches": args.steps,
-            "clocks": clk,
-            "finite_output": ok,
-        }
-        if world == 1 and not args.no_extras:
-            try:
-                line["configs"] = other_configs(torch, peak)
-            except Exception as exc:  # never lose the headline line
-                line["configs"] = {"error": repr(exc)}
-        if world == 1 and not args.no_cpu_baseline:
-            cores = host_cores()
-            per_core = args.ref_products_per_core
-            rate, total, wall = cpu_reference_rate(per_core, cores)
-            line["cpu_baseline"] = {
-                "value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                "sample": f"{total} products ({per_core}/core), exact L=d_H=4093, "
-                          f"wall {wall:.2f}s"}
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
-    return 0
+# ---------------------------------------------------------------- launcher
+def relaunch(args):
+    """``--gpus N`` outside torchrun: re-launch under torch.distributed.run,
+    one process per GPU, rendezvous on 127.0.0.1."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -450,13 +687,22 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--ref-products-per-core", type=int, default=1024)
+    ap.add_argument("--engine", default="",
+                    help="module:Class of an alternative product engine (tests use a CPU "
+                         "engine to drive the multi-rank harness over gloo)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-quick", action="store_true",
+                    help="cfg2-only CPU baseline (skip the per-config CPU columns)")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the cfg1/3/4/5 side measurements")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-products-per-core", type=int, default=0,
+                    help="(kept for compatibility; the CPU legs time the full batch)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     return run_ours(args)
 
 

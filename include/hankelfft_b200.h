@@ -38,13 +38,19 @@ extern "C" {
 #define HK_C128 0 /* complex128 vector / matrix                                  */
 #define HK_F64 1  /* float64 (real) vector; promoted to complex like core.as_complex */
 #define HK_SPEC 2 /* spectrum previously produced by hk_spectrum / hk_vector_spectra */
+/* Single-precision variant (north_star: rel. error <= 1e-4).  A product whose
+ * h is HK_C64 / HK_F32 takes only HK_C64 / HK_F32 vectors, computes in FP32 and
+ * writes complex64 y / alpha; on-chip plans (L <= 8192), hk_tvp_partial and
+ * hk_tvp_full only.  The reference itself is complex128-only (core.py:21-22). */
+#define HK_C64 3  /* complex64 vector                                             */
+#define HK_F32 4  /* float32 (real) vector, promoted to complex64                 */
 
 /* One operand of a product: a batch of vectors (or spectra) in device memory.
  * Item b of the batch starts at data + b * batch_stride elements. */
 typedef struct hk_operand {
   const void *data;
   int64_t batch_stride;
-  int32_t dtype; /* HK_C128 | HK_F64 | HK_SPEC */
+  int32_t dtype; /* HK_C128 | HK_F64 | HK_SPEC | HK_C64 | HK_F32 */
   int32_t reserved;
 } hk_operand;
 
@@ -97,7 +103,8 @@ int hk_spectrum(const hk_plan *plan, hk_operand h, int64_t batch, void *spec, vo
  * (HK_SPEC).  xs has order-1 operands, xs[p] for mode p+2 (length n_{p+2}).
  * Operands with identical (data, batch_stride, dtype) are transformed once and
  * raised to their multiplicity (H x^{m-1} costs one vector transform).
- * y: complex128, item b at y + b * y_stride elements, n_1 values. */
+ * y: complex128 (complex64 for HK_C64/HK_F32 operands), item b at
+ * y + b * y_stride elements, n_1 values. */
 int hk_tvp_partial(const hk_plan *plan, hk_operand h, const hk_operand *xs, int nx,
                    int64_t batch, void *y, int64_t y_stride, void *workspace, void *stream);
 
@@ -115,7 +122,8 @@ int hk_tvp_partial_host(const hk_plan *plan, hk_operand h, const void *host_in, 
 
 /* alpha = H x_1 ... x_m (unconjugated): HankelTensor.tvp_full
  * (hankel.py:149-154) / AntiCirculantTensor.tvp_full (hankel.py:47-59).
- * xs has `order` operands.  alpha: complex128[batch] (stride 1). */
+ * xs has `order` operands.  alpha: complex128[batch] (stride 1); complex64
+ * for HK_C64/HK_F32 operands. */
 int hk_tvp_full(const hk_plan *plan, hk_operand h, const hk_operand *xs, int nx, int64_t batch,
                 void *alpha, void *workspace, void *stream);
 

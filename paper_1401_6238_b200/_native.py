@@ -20,6 +20,8 @@ HK_EUNSUPPORTED = -4
 HK_C128 = 0
 HK_F64 = 1
 HK_SPEC = 2
+HK_C64 = 3
+HK_F32 = 4
 
 LIB_NAME = "libhankelfft_b200.so"
 LIB_PATH = os.environ.get("HK_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)

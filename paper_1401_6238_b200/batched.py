@@ -3,7 +3,11 @@
 Every function here launches the sm_100a kernels of ``libhankelfft_b200.so``
 asynchronously on the current torch CUDA stream and returns device tensors;
 nothing synchronises.  Inputs are complex128 (or float64, promoted on the fly
-like the reference's ``core.as_complex``, core.py:21-22).
+like the reference's ``core.as_complex``, core.py:21-22).  The products also
+take complex64 / float32 operands (all of them single precision): FP32
+arithmetic, complex64 results, relative error <= 1e-4 (the north_star's fp32
+tolerance); on-chip lengths (d_H <= 8192), ``hankel_tvp_partial`` and
+``hankel_tvp_full``.
 
 Shapes (B = batch of independent tensors):
   h     : (B, d_H) generating vectors, or (B, L) spectra from ``hankel_spectrum``
@@ -48,9 +52,19 @@ def _operand(t: torch.Tensor, name: str, spectrum: bool = False) -> N.Operand:
         dt = N.HK_SPEC if spectrum else N.HK_C128
     elif t.dtype == torch.float64 and not spectrum:
         dt = N.HK_F64
+    elif t.dtype == torch.complex64 and not spectrum:
+        dt = N.HK_C64
+    elif t.dtype == torch.float32 and not spectrum:
+        dt = N.HK_F32
     else:
-        raise ValueError(f"{name} must be complex128{'' if spectrum else ' or float64'}")
+        raise ValueError(f"{name} must be complex128{'' if spectrum else ', float64, complex64 or float32'}")
     return N.Operand(t.data_ptr(), t.stride(0), dt, 0)
+
+
+def _out_dtype(h: torch.Tensor):
+    """complex64 results for the single-precision variant (h complex64 / float32,
+    FP32 arithmetic, north_star tolerance 1e-4), complex128 otherwise."""
+    return torch.complex64 if h.dtype in (torch.complex64, torch.float32) else torch.complex128
 
 
 def _stream(device) -> ctypes.c_void_p:
@@ -161,8 +175,10 @@ def hankel_tvp_partial(h: torch.Tensor, xs, shape, *, spectrum: bool = False,
     with _OnDevice(dev):
         plan = hankel_plan(shape, dev, fft_len)
         if out is None:
-            out = torch.empty((B, shape[0]), dtype=torch.complex128, device=h.device)
+            out = torch.empty((B, shape[0]), dtype=_out_dtype(h), device=h.device)
         _require_cuda(out, "out")
+        if out.dtype != _out_dtype(h) or out.stride(-1) != 1:
+            raise ValueError(f"out must be a {_out_dtype(h)} tensor contiguous along its rows")
         ops = _vector_operands(xs, [f"xs[{i}]" for i in range(len(xs))])
         ws = _workspace(plan, B, h.device)
         N.check(N.load_library().hk_tvp_partial(
@@ -184,7 +200,7 @@ def hankel_tvp_full(h: torch.Tensor, xs, shape, *, spectrum: bool = False,
     B = h.shape[0]
     with _OnDevice(dev):
         plan = hankel_plan(shape, dev, fft_len)
-        alpha = torch.empty((B,), dtype=torch.complex128, device=h.device)
+        alpha = torch.empty((B,), dtype=_out_dtype(h), device=h.device)
         ops = _vector_operands(xs, [f"xs[{i}]" for i in range(len(xs))])
         ws = _workspace(plan, B, h.device)
         N.check(N.load_library().hk_tvp_full(
@@ -329,6 +345,53 @@ def bhhb_tvp_full(H: torch.Tensor, xs, order, block_shape, outer_shape) -> torch
                                              alpha.data_ptr(), ws.data_ptr(), _stream(dev)),
                 "hk_tvp_full(block)")
     return alpha
+
+
+def hankel_tvp_partial_multi(h: torch.Tensor, xs, shape, *, devices=None, gather_to=None,
+                             fft_len: int = 0):
+    """Batched H x_2 ... x_m sharded over several GPUs from ONE process
+    (SURVEY §8e): contiguous shards of the batch (``dist.shard_range``), each
+    launched on its device's current stream with no cross-device traffic
+    except moving the shard's inputs there and -- only when ``gather_to`` is
+    given -- the results back (peer copies over NVLink).
+
+    h: (B, d_H), xs[p]: (B, n_{p+2}) on the host (pinned for async copies) or on
+    any CUDA device; the same tensor object twice means the same vector.
+    ``devices``: list of CUDA device indices (default: all visible).
+    Returns the list of per-device (B_k, n_1) outputs (a Shard(0) layout), or
+    one (B, n_1) tensor on ``gather_to``.  Nothing synchronises.
+    """
+    from .dist import shard_range
+
+    shape = tuple(int(n) for n in shape)
+    xs = list(xs)
+    if len(xs) != len(shape) - 1:
+        raise ValueError(f"expected {len(shape) - 1} vectors, got {len(xs)}")
+    devices = list(range(torch.cuda.device_count())) if devices is None else list(devices)
+    if not devices:
+        raise RuntimeError("no CUDA device: the product path runs only on the GPU")
+    B = h.shape[0]
+    outs = []
+    for k, dev in enumerate(devices):
+        lo, hi = shard_range(B, k, len(devices))
+        with torch.cuda.device(dev):
+            if hi == lo:
+                outs.append(torch.empty((0, shape[0]), dtype=torch.complex128,
+                                        device=f"cuda:{dev}"))
+                continue
+            hs = h[lo:hi].to(f"cuda:{dev}", non_blocking=True)
+            moved = {}
+            xsd = []
+            for x in xs:
+                if id(x) not in moved:
+                    moved[id(x)] = x[lo:hi].to(f"cuda:{dev}", non_blocking=True)
+                xsd.append(moved[id(x)])
+            outs.append(hankel_tvp_partial(hs, xsd, shape, fft_len=fft_len))
+    if gather_to is None:
+        return outs
+    dst = torch.device(gather_to) if not isinstance(gather_to, int) else \
+        torch.device("cuda", gather_to)
+    return torch.cat([o.to(dst, non_blocking=True) for o in outs], dim=0)
 
 
 class _HostPipeline:

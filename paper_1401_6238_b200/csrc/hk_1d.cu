@@ -144,33 +144,6 @@ static cudaError_t launch_plan(const Args1D &a, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-// Supported on-chip lengths.  Power-of-two lengths use radix-16 passes with one
-// small leading radix; 3*2^k lengths put a radix-12/24/3/6 pass first.
-#define HK_PLAN_LIST(X)                     \
-  X(2, Plan1D<2, 1, 2>)                     \
-  X(4, Plan1D<4, 1, 4>)                     \
-  X(8, Plan1D<8, 1, 8>)                     \
-  X(16, Plan1D<16, 1, 16>)                  \
-  X(32, Plan1D<32, 2, 2, 16>)               \
-  X(64, Plan1D<64, 4, 4, 16>)               \
-  X(128, Plan1D<128, 8, 8, 16>)             \
-  X(256, Plan1D<256, 16, 16, 16>)           \
-  X(512, Plan1D<512, 32, 2, 16, 16>)        \
-  X(1024, Plan1D<1024, 64, 4, 16, 16>)      \
-  X(2048, Plan1D<2048, 128, 8, 16, 16>)     \
-  X(4096, Plan1D<4096, 256, 16, 16, 16>)    \
-  X(8192, Plan1D<8192, 512, 2, 16, 16, 16>) \
-  X(12, Plan1D<12, 1, 12>)                  \
-  X(24, Plan1D<24, 1, 24>)                  \
-  X(48, Plan1D<48, 3, 3, 16>)               \
-  X(96, Plan1D<96, 6, 6, 16>)               \
-  X(192, Plan1D<192, 12, 12, 16>)           \
-  X(384, Plan1D<384, 24, 24, 16>)           \
-  X(768, Plan1D<768, 48, 3, 16, 16>)        \
-  X(1536, Plan1D<1536, 96, 6, 16, 16>)      \
-  X(3072, Plan1D<3072, 192, 12, 16, 16>)    \
-  X(6144, Plan1D<6144, 384, 24, 16, 16>)
-
 cudaError_t launch_1d(int L, const Args1D &a, cudaStream_t stream) {
   switch (L) {
 #define HK_CASE(len, ...) \

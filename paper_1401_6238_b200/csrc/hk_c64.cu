@@ -1,0 +1,427 @@
+// complex64 / float32 variant of the fused batched 1D Hankel products
+// (north_star: relative error <= 1e-4 for fp32/complex64).  Same algorithm
+// as the complex128 kernels (reference hankel.py:140-154 via the
+// anti-circulant embedding, hankel.py:42-71), FP32 arithmetic throughout:
+//   acc = ifft(h~)                 (pass 0 reads the nonzero h prefix only)
+//   acc *= fft(x~_f)^{power_f}     (one transform per DISTINCT vector; the
+//                                   reference's multiplication order)
+//   partial: y = fft(acc)[:n_1]    (transposed network, natural-order output)
+//   full:    alpha = sum(acc)      (fixed-order reduction)
+// The reference itself is complex128-only (core.py:21-22); this is the
+// batched-API extension SURVEY §7 step 8 / §8(b) list as HK_C64 / HK_F32.
+//
+// Design: half the bytes of a complex128 working set, so the accumulator and
+// one vector spectrum both stay in registers (no TMEM needed) and the FP32
+// pipe (2x the FP64 rate on B200) does the butterflies.  Latency is hidden by
+// occupancy: several independent products per SM, each a CTA group of T
+// threads exchanging through its own 8-byte-swizzled shared-memory buffer.
+// Twiddles come from an L1-resident single-precision table computed in long
+// double on the host.
+#include <atomic>
+#include <stdlib.h>
+
+#include "hk_fastcore.cuh"
+#include "hk_fft1d.cuh"
+#include "hk_internal.h"
+#include "hk_tmem.cuh"
+
+#ifndef HK_C64_MINB
+#define HK_C64_MINB 4  // resident CTAs/SM of the 256-thread fast complex64 kernel
+#endif
+
+namespace hk {
+
+using cplxf = float2;
+
+__device__ __forceinline__ cplxf ld_c64(const Factor &f, long long off, int pos, float scale) {
+  if (pos >= f.len) return make_float2(0.f, 0.f);
+  const long long k = (long long)pos * f.estride;
+  if (f.kind == FK_F32) {
+    const float *p = static_cast<const float *>(f.ptr) + off;
+    return make_float2(__ldg(p + k) * scale, 0.f);
+  }
+  const cplxf *p = static_cast<const cplxf *>(f.ptr) + off;
+  const cplxf v = __ldg(p + k);
+  return make_float2(v.x * scale, v.y * scale);
+}
+
+// The accumulator lives in TMEM (as in the complex128 fast kernel) for plans
+// with V >= 8 values per thread, so only one length-L working set is in
+// registers while the next spectrum is computed; tiny plans keep it in
+// registers.  Warp w owns TMEM lanes 32*(w%4).. and a 2V-column slab w/4.
+template <class PL>
+struct C64Tr {
+  static constexpr bool tmem = PL::V >= 8 && PL::V % 4 == 0;
+  static constexpr int warps = PL::CTA / 32;
+  static constexpr int slabs = (warps + 3) / 4;
+  static constexpr int need = slabs * 2 * PL::V;
+  static constexpr int cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : 256;
+  static constexpr int min_blocks = PL::CTA >= 384 ? 1 : 2;
+};
+
+template <class PL>
+__global__ void __launch_bounds__(PL::CTA, (C64Tr<PL>::min_blocks))
+    k_hankel_c64(const __grid_constant__ Args1D a) {
+  using Tr = C64Tr<PL>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint32_t tmem_slot;
+  cplxf *smem = reinterpret_cast<cplxf *>(smem_raw);
+  constexpr int T = PL::T;
+  constexpr int V = PL::V;
+  const int g = threadIdx.x / T;
+  const int t = threadIdx.x - g * T;
+  const int warp = threadIdx.x >> 5;
+  cplxf *sbuf = smem + (PL::P > 1 ? g * PL::L : 0);
+  const cplxf *__restrict__ tw = a.twf;
+  const long long nblk = (a.batch + PL::G - 1) / PL::G;
+  uint32_t tmy = 0;
+  if constexpr (Tr::tmem) {
+    if (warp == 0) tmem_alloc<Tr::cols>(&tmem_slot);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    tmy = tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 2 * V);
+  }
+
+  for (long long bb = blockIdx.x; bb < nblk; bb += gridDim.x) {
+    long long b = bb * PL::G + g;
+    const bool active = b < a.batch;
+    if (!active) b = a.batch - 1;  // idle groups shadow a valid item; stores are masked
+    const long long ob = b / a.nsub, os = b - ob * a.nsub;
+
+    cplxf acc[Tr::tmem ? 1 : V];
+    cplxf v[V];
+    {
+      const Factor &hf = a.h;
+      const float sc = (float)a.scale;
+      const long long off = ob * hf.bstride + os * hf.sstride;
+      fft_dif<PL, true>(sbuf, t, tw, [&](int pos) { return ld_c64(hf, off, pos, sc); }, v);
+      if constexpr (Tr::tmem) {
+        tmem_wait_st();  // the previous item's reads of TMEM are complete
+#pragma unroll
+        for (int c = 0; c < V / 4; ++c) tmem_st4f(tmy + 8 * c, &v[4 * c]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < V; ++r) acc[r] = v[r];
+      }
+    }
+    for (int f = 0; f < a.nfac; ++f) {
+      const Factor &fa = a.fac[f];
+      const long long off = ob * fa.bstride + os * fa.sstride;
+      fft_dif<PL, false>(sbuf, t, tw, [&](int pos) { return ld_c64(fa, off, pos, 1.f); }, v);
+      if constexpr (Tr::tmem) {
+        tmem_wait_st();
+#pragma unroll
+        for (int c = 0; c < V / 4; ++c) {
+          cplxf q[4];
+          tmem_ld4f(tmy + 8 * c, q);
+          for (int k = 0; k < fa.power; ++k) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) q[i] = cmul(q[i], v[4 * c + i]);
+          }
+          tmem_st4f(tmy + 8 * c, q);
+        }
+      } else {
+        for (int k = 0; k < fa.power; ++k) {
+#pragma unroll
+          for (int r = 0; r < V; ++r) acc[r] = cmul(acc[r], v[r]);
+        }
+      }
+    }
+    if constexpr (Tr::tmem) {
+      tmem_wait_st();
+#pragma unroll
+      for (int c = 0; c < V / 4; ++c) tmem_ld4f(tmy + 8 * c, &v[4 * c]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < V; ++r) v[r] = acc[r];
+    }
+    cplxf *out = static_cast<cplxf *>(a.out) + ob * a.out_bstride + os * a.out_sstride;
+    if (a.mode == M_PARTIAL) {
+      const int n1 = a.out_len;
+      const long long es = a.out_estride;
+      fft_dit_final<PL>(sbuf, t, tw, v, [&](int pos, cplxf y) {
+        if (active && pos < n1) out[pos * es] = y;
+      });
+    } else {
+      cplxf s = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int r = 0; r < V; ++r) s = cadd(s, v[r]);
+      __syncthreads();
+      cplxf *red = smem + g * T;  // G*T <= G*L slots
+      red[t] = s;
+      __syncthreads();
+      if (t == 0 && active) {
+        cplxf tot = make_float2(0.f, 0.f);
+        for (int k = 0; k < T; ++k) tot = cadd(tot, red[k]);
+        out[0] = tot;
+      }
+    }
+    __syncthreads();  // the exchange buffers are reused by the next item
+  }
+  if constexpr (Tr::tmem) {
+    tmem_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+      tmem_fence_after();
+      tmem_dealloc<Tr::cols>(tmem_slot);
+    }
+  }
+}
+
+// Resident CTAs on the whole GPU for a persistent grid, from the register,
+// shared-memory and thread limits (the occupancy API under-reports for these
+// kernels, as for the complex128 fast kernel: it returned 1 CTA/SM here).
+static int resident_ctas(const void *fn, int cta, int smem, int dev) {
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, fn);
+  int sms = 0, smem_sm = 0, regs_sm = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+  int per = regs_sm / (((fa.numRegs + 7) / 8 * 8) * cta);
+  const int by_smem = smem_sm / (smem + (int)fa.sharedSizeBytes + 1024);
+  per = per < by_smem ? per : by_smem;
+  per = per < 2048 / cta ? per : 2048 / cta;
+  return sms * (per > 0 ? per : 1);
+}
+
+// ---------------------------------------------------------------------------
+// Fast variant for the batched lengths (the complex128 fast kernel's engine,
+// hk_fastcore.cuh, instantiated on float2): pruned first/last passes,
+// recurrence twiddles from one table read per butterfly, 8-byte swizzled
+// exchanges, TMEM accumulator, L2 prefetch of the next block's operands.
+__device__ __forceinline__ void prefetch_f(const Factor &f, long long b, long long nsub) {
+  if (f.estride != 1 || f.len <= 0) return;
+  const int eb = f.kind == FK_F32 ? 4 : 8;
+  const long long ob = b / nsub, os = b - ob * nsub;
+  const char *p = static_cast<const char *>(f.ptr) + (ob * f.bstride + os * f.sstride) * eb;
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+  const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p) + (unsigned)f.len * eb + 15) &
+                       ~(uintptr_t)15;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a0), "r"((unsigned)(a1 - a0))
+               : "memory");
+}
+
+template <class PL>
+struct FastC64Tr {
+  static constexpr int warps = PL::CTA / 32;
+  static constexpr int slabs = (warps + 3) / 4;
+  static constexpr int need = slabs * 2 * PL::V;
+  static constexpr int cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : 256;
+  static constexpr int min_blocks = PL::CTA >= 512 ? 1 : (PL::CTA >= 384 ? 2 : HK_C64_MINB);
+};
+
+template <class PL, int NZ, int NO>
+__global__ void __launch_bounds__(PL::CTA, (FastC64Tr<PL>::min_blocks))
+    k_hankel_fast_c64(const __grid_constant__ Args1D a) {
+  using Tr = FastC64Tr<PL>;
+  constexpr int T = PL::T;
+  constexpr int V = PL::V;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint32_t tmem_slot;
+  cplxf *smem = reinterpret_cast<cplxf *>(smem_raw);
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc<Tr::cols>(&tmem_slot);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tmy =
+      tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 2 * V);
+  const int g = threadIdx.x / T;
+  const int t = threadIdx.x - g * T;
+  const long long nblk = (a.batch + PL::G - 1) / PL::G;
+  cplxf *sbuf = smem + g * PL::L;
+  const cplxf *__restrict__ tw = a.twf;
+  const fast::Tw0RecT<cplxf> tw0{a.twf};
+  const fast::GroupSync<PL> gsync;
+  auto prefetch = [&](long long bb) {
+    for (int q = 0; q < PL::G; ++q) {
+      const long long b = bb * PL::G + q;
+      if (b >= a.batch) break;
+      prefetch_f(a.h, b, a.nsub);
+      for (int f = 0; f < a.nfac; ++f) prefetch_f(a.fac[f], b, a.nsub);
+    }
+  };
+  if (a.prefetch && threadIdx.x == 0) prefetch(blockIdx.x);
+
+  for (long long bb = blockIdx.x; bb < nblk; bb += gridDim.x) {
+    if constexpr (std::is_same_v<fast::GroupSync<PL>, fast::WarpSync>) {
+      if (bb != blockIdx.x) __syncthreads();
+    }
+    if (a.prefetch && threadIdx.x == 0 && bb + gridDim.x < nblk) prefetch(bb + gridDim.x);
+    long long b = bb * PL::G + g;
+    const bool active = b < a.batch;
+    if (!active) b = a.batch - 1;
+    const long long ob = b / a.nsub, os = b - ob * a.nsub;
+    cplxf v[V];
+    {
+      const Factor &hf = a.h;
+      const long long off = ob * hf.bstride + os * hf.sstride;
+      const float sc = (float)a.scale;
+      fast::fft_dif<PL, true, PL::radix[0], PL::L, true>(
+          sbuf, t, tw, tw0, [&](int pos) { return fast::load_elem_f(hf, off, pos, sc); }, v,
+          gsync);
+      tmem_wait_st();
+#pragma unroll
+      for (int c = 0; c < V / 4; ++c) tmem_st4f(tmy + 8 * c, &v[4 * c]);
+    }
+    for (int f = 0; f < a.nfac; ++f) {
+      const Factor &fa = a.fac[f];
+      const long long off = ob * fa.bstride + os * fa.sstride;
+      fast::fft_dif<PL, false, NZ, PL::L, true>(
+          sbuf, t, tw, tw0, [&](int pos) { return fast::load_elem_f(fa, off, pos, 1.f); }, v,
+          gsync);
+      tmem_wait_st();
+#pragma unroll
+      for (int c = 0; c < V / 4; ++c) {
+        cplxf q[4];
+        tmem_ld4f(tmy + 8 * c, q);
+        for (int k = 0; k < fa.power; ++k) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) q[i] = cmul(q[i], v[4 * c + i]);
+        }
+        tmem_st4f(tmy + 8 * c, q);
+      }
+    }
+    tmem_wait_st();
+#pragma unroll
+    for (int c = 0; c < V / 4; ++c) tmem_ld4f(tmy + 8 * c, &v[4 * c]);
+    cplxf *out = static_cast<cplxf *>(a.out) + ob * a.out_bstride + os * a.out_sstride;
+    if (a.mode == M_PARTIAL) {
+      const int n1 = a.out_len;
+      const long long es = a.out_estride;
+      fast::fft_final<PL, NO, PL::L, true>(
+          sbuf, t, tw, tw0, v,
+          [&](int pos, cplxf y) {
+            if (active && pos < n1) out[pos * es] = y;
+          },
+          gsync);
+    } else {
+      cplxf s = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int r = 0; r < V; ++r) s = cadd(s, v[r]);
+      gsync();
+      cplxf *red = sbuf;
+      red[t] = s;
+      gsync();
+      if (t == 0 && active) {
+        cplxf tot = make_float2(0.f, 0.f);
+        for (int k = 0; k < T; ++k) tot = cadd(tot, red[k]);
+        out[0] = tot;
+      }
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tmem_fence_after();
+    tmem_dealloc<Tr::cols>(tmem_slot);
+  }
+}
+
+template <class PL, int NZ, int NO>
+static cudaError_t launch_fast_c64_variant(const Args1D &a, cudaStream_t stream) {
+  const int smem = PL::G * PL::L * (int)sizeof(cplxf) + 128;
+  static std::atomic<unsigned long long> configured{0};
+  static int resident[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(configured.load() & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(k_hankel_fast_c64<PL, NZ, NO>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    // carve out shared memory for every resident CTA (TMEM holds the accumulators)
+    e = cudaFuncSetAttribute(k_hankel_fast_c64<PL, NZ, NO>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+    resident[dev & 63] = resident_ctas(reinterpret_cast<const void *>(
+                                           k_hankel_fast_c64<PL, NZ, NO>),
+                                       PL::CTA, smem, dev);
+    configured.fetch_or(bit);
+  }
+  const long long nblk = (a.batch + PL::G - 1) / PL::G;
+  if (nblk <= 0) return cudaSuccess;
+  const long long grid = nblk < resident[dev & 63] ? nblk : resident[dev & 63];
+  k_hankel_fast_c64<PL, NZ, NO><<<(unsigned)grid, PL::CTA, smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+// pruning levels: nonzero first-pass inputs / needed last-pass outputs per
+// butterfly, rounded up to the instantiated levels {R0/4, R0/2, R0}
+template <class PL>
+static cudaError_t launch_fast_c64(const Args1D &a, cudaStream_t stream, int maxlen, int outl) {
+  constexpr int R0 = PL::radix[0], S0 = PL::stride(0);
+  constexpr int q = R0 >= 4 ? R0 / 4 : 1, h = R0 >= 2 ? R0 / 2 : 1;
+  const int nz = (maxlen + S0 - 1) / S0, no = (outl + S0 - 1) / S0;
+  const int zi = nz <= q ? 0 : (nz <= h ? 1 : 2), oi = no <= q ? 0 : (no <= h ? 1 : 2);
+  switch (zi * 3 + oi) {
+    case 0: return launch_fast_c64_variant<PL, q, q>(a, stream);
+    case 1: return launch_fast_c64_variant<PL, q, h>(a, stream);
+    case 2: return launch_fast_c64_variant<PL, q, R0>(a, stream);
+    case 3: return launch_fast_c64_variant<PL, h, q>(a, stream);
+    case 4: return launch_fast_c64_variant<PL, h, h>(a, stream);
+    case 5: return launch_fast_c64_variant<PL, h, R0>(a, stream);
+    case 6: return launch_fast_c64_variant<PL, R0, q>(a, stream);
+    case 7: return launch_fast_c64_variant<PL, R0, h>(a, stream);
+    default: return launch_fast_c64_variant<PL, R0, R0>(a, stream);
+  }
+}
+
+template <class PL>
+static cudaError_t launch_c64_plan(const Args1D &a, cudaStream_t stream) {
+  int smem = (PL::P > 1) ? PL::G * PL::L * (int)sizeof(cplxf) : 16;
+  const int red_bytes = PL::G * PL::T * (int)sizeof(cplxf);
+  if (smem < red_bytes) smem = red_bytes;
+  static std::atomic<unsigned long long> configured{0};
+  static int resident[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(configured.load() & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(k_hankel_c64<PL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    resident[dev & 63] =
+        resident_ctas(reinterpret_cast<const void *>(k_hankel_c64<PL>), PL::CTA, smem, dev);
+    configured.fetch_or(bit);
+  }
+  const long long nblk = (a.batch + PL::G - 1) / PL::G;
+  if (nblk <= 0) return cudaSuccess;
+  const long long grid = nblk < resident[dev & 63] ? nblk : resident[dev & 63];
+  k_hankel_c64<PL><<<(unsigned)grid, PL::CTA, smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_c64_1d(int L, const Args1D &a, cudaStream_t stream) {
+  if (!a.twf) return cudaErrorInvalidValue;
+  if (a.mode != M_PARTIAL && a.mode != M_FULL) return cudaErrorNotSupported;
+  static const bool generic_only = getenv("HK_C64_GENERIC") != nullptr;  // A/B switch
+  if (!generic_only) {
+    int maxlen = 1;
+    for (int f = 0; f < a.nfac; ++f)
+      if (a.fac[f].len > maxlen) maxlen = a.fac[f].len;
+    const int outl = a.mode == M_PARTIAL ? a.out_len : L;
+    switch (L) {
+      case 4096: return launch_fast_c64<Plan1D<4096, 256, 16, 16, 16>>(a, stream, maxlen, outl);
+      case 8192: return launch_fast_c64<Plan1D<8192, 512, 2, 16, 16, 16>>(a, stream, maxlen, outl);
+      case 2048: return launch_fast_c64<Plan1D<2048, 128, 8, 16, 16>>(a, stream, maxlen, outl);
+      case 1024: return launch_fast_c64<Plan1D<1024, 64, 4, 16, 16>>(a, stream, maxlen, outl);
+      case 256: return launch_fast_c64<Plan1D<256, 16, 16, 16>>(a, stream, maxlen, outl);
+      default: break;
+    }
+  }
+  switch (L) {
+#define HK_CASE(len, ...) \
+  case len:              \
+    return launch_c64_plan<__VA_ARGS__>(a, stream);
+    HK_PLAN_LIST(HK_CASE)
+#undef HK_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace hk

@@ -32,6 +32,7 @@ struct hk_plan {
   const double2 *tw = nullptr;  // 1D twiddle table (length L[0])
   const double2 *tw0 = nullptr; // thread-major first-pass table for the fast kernels
   const double2 *tw1 = nullptr; // compact W_{L/R0} table for passes >= 1 (fast kernels)
+  const float2 *twf = nullptr;  // single-precision W_L table (complex64 variant)
   // two-level plans (large 1D four-step or 2D block): L1 columns x L2 rows
   int two_level = 0;
   int twiddle = 0;               // 1D four-step (1) or 2D block (0)
@@ -95,6 +96,40 @@ int get_twiddles(int device, long long L, const double2 **out) {
     return cuda_fail(err, "cudaMemcpy(twiddles)");
   }
   g_tw[key] = d;
+  *out = d;
+  return HK_OK;
+}
+
+// Single-precision W_L^e (complex64 variant), rounded from long double.
+std::map<std::pair<int, long long>, float2 *> g_twf;
+
+int get_twiddles_f(int device, long long L, const float2 **out) {
+  std::lock_guard<std::mutex> lk(g_tw_mu);
+  auto key = std::make_pair(device, L);
+  auto it = g_twf.find(key);
+  if (it != g_twf.end()) {
+    *out = it->second;
+    return HK_OK;
+  }
+  std::vector<float2> host(L);
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  for (long long e = 0; e < L; ++e) {
+    long double ang = two_pi * (long double)e / (long double)L;
+    host[e].x = (float)cosl(ang);
+    host[e].y = (float)-sinl(ang);
+    if (4 * e == L) host[e] = make_float2(0.f, -1.f);
+    if (2 * e == L) host[e] = make_float2(-1.f, 0.f);
+    if (4 * e == 3 * L) host[e] = make_float2(0.f, 1.f);
+  }
+  float2 *d = nullptr;
+  cudaError_t err = cudaMalloc(&d, L * sizeof(float2));
+  if (err != cudaSuccess) return cuda_fail(err, "cudaMalloc(twiddles f32)");
+  err = cudaMemcpy(d, host.data(), L * sizeof(float2), cudaMemcpyHostToDevice);
+  if (err != cudaSuccess) {
+    cudaFree(d);
+    return cuda_fail(err, "cudaMemcpy(twiddles f32)");
+  }
+  g_twf[key] = d;
   *out = d;
   return HK_OK;
 }
@@ -234,6 +269,8 @@ int operand_kind(int32_t dtype, int32_t *kind) {
     case HK_C128: *kind = hk::FK_C128; return HK_OK;
     case HK_F64: *kind = hk::FK_F64; return HK_OK;
     case HK_SPEC: *kind = hk::FK_SPEC; return HK_OK;
+    case HK_C64: *kind = hk::FK_C64; return HK_OK;
+    case HK_F32: *kind = hk::FK_F32; return HK_OK;
     default: return fail(HK_EINVAL, "unknown operand dtype %d", dtype);
   }
 }
@@ -257,6 +294,7 @@ Args1D base_args(const hk_plan *p, int64_t batch) {
   a.tw = p->tw;
   a.tw0 = p->tw0;
   a.tw1 = p->tw1;
+  a.twf = p->twf;
   a.scale = 1.0 / (double)p->L[0];
   a.out_estride = 1;
   a.prefetch = getenv("HK_NO_PREFETCH") ? 0 : 1;
@@ -298,6 +336,30 @@ int set_vectors(const hk_plan *p, const hk_operand *xs, int nx, int mode_offset,
                   hk::kMaxFactors);
     a.fac[a.nfac++] = make_factor(xs[i], kind, len, p->L[0]);
   }
+  return HK_OK;
+}
+
+bool single_kind(int32_t dtype) { return dtype == HK_C64 || dtype == HK_F32; }
+
+// complex64 variant: every operand single precision, on-chip plan, no spectra.
+int check_single(const hk_plan *p, const hk_operand &h, const hk_operand *xs, int nx) {
+  if (!single_kind(h.dtype)) {
+    for (int i = 0; i < nx; ++i)
+      if (single_kind(xs[i].dtype))
+        return fail(HK_EINVAL, "vector %d is single precision but h is not (mixed precision)", i);
+    return 0;
+  }
+  for (int i = 0; i < nx; ++i)
+    if (!single_kind(xs[i].dtype))
+      return fail(HK_EINVAL, "vector %d must be HK_C64/HK_F32 when h is single precision", i);
+  if (p->two_level || !p->twf)
+    return fail(HK_EUNSUPPORTED, "the complex64 variant covers on-chip plans (L <= 8192)");
+  return 1;
+}
+
+int launch_single(const hk_plan *p, const Args1D &a, void *stream) {
+  cudaError_t e = hk::launch_c64_1d((int)p->L[0], a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "complex64 kernel launch");
   return HK_OK;
 }
 
@@ -349,6 +411,7 @@ int hk_plan_create_hankel(hk_plan **plan, int order, const int64_t *mode_sizes, 
   if (L > 0 && hk::supported_1d(L)) {
     p->L = {L};
     rc = line_tables(dev, L, &p->tw, &p->tw0, &p->tw1);
+    if (!rc) rc = get_twiddles_f(dev, L, &p->twf);
   } else {
     // two-level four-step: L = L1 * L2 (L1 column plan, L2 fast row plan)
     long long best1 = 0, best2 = 0;
@@ -844,6 +907,8 @@ int hk_spectrum(const hk_plan *plan, hk_operand h, int64_t batch, void *spec, vo
   if (batch < 0) return fail(HK_EINVAL, "negative batch");
   if (batch == 0) return HK_OK;
   if (h.dtype == HK_SPEC) return fail(HK_EINVAL, "h is already a spectrum");
+  if (single_kind(h.dtype))
+    return fail(HK_EUNSUPPORTED, "cached spectra exist for complex128 only");
   if (!spec) return fail(HK_EINVAL, "spec is NULL");
   if (plan->two_level) return tl_run(plan, h, nullptr, 0, 0, batch, spec, 0, workspace, stream, 2);
   Args1D a = base_args(plan, batch);
@@ -865,6 +930,9 @@ int hk_tvp_partial(const hk_plan *plan, hk_operand h, const hk_operand *xs, int 
   if (batch < 0) return fail(HK_EINVAL, "negative batch");
   if (batch == 0) return HK_OK;
   if (!y) return fail(HK_EINVAL, "y is NULL");
+  if (!xs) return fail(HK_EINVAL, "xs is NULL");
+  const int single = check_single(plan, h, xs, nx);
+  if (single < 0) return single;
   if (plan->two_level) return tl_run(plan, h, xs, nx, 1, batch, y, y_stride, workspace, stream, 0);
   Args1D a = base_args(plan, batch);
   if ((rc = set_h(plan, h, a))) return rc;
@@ -873,7 +941,7 @@ int hk_tvp_partial(const hk_plan *plan, hk_operand h, const hk_operand *xs, int 
   a.out = y;
   a.out_bstride = y_stride;
   a.out_len = (int32_t)plan->sizes[0];
-  return launch(plan, a, stream);
+  return single ? launch_single(plan, a, stream) : launch(plan, a, stream);
 }
 
 int hk_tvp_partial_host(const hk_plan *plan, hk_operand h, const void *host_in, int64_t in_elems,
@@ -882,6 +950,7 @@ int hk_tvp_partial_host(const hk_plan *plan, hk_operand h, const void *host_in, 
   int rc = check_plan(plan);
   if (rc) return rc;
   if (plan->two_level) return fail(HK_EUNSUPPORTED, "host latency path covers on-chip plans only");
+  if (single_kind(h.dtype)) return fail(HK_EUNSUPPORTED, "host latency path is complex128 only");
   if (nx != plan->order - 1)
     return fail(HK_EINVAL, "expected %d vectors, got %d", plan->order - 1, nx);
   if (nx > hk::kMaxFactors) return fail(HK_EUNSUPPORTED, "too many vectors");
@@ -931,6 +1000,9 @@ int hk_tvp_full(const hk_plan *plan, hk_operand h, const hk_operand *xs, int nx,
   if (batch < 0) return fail(HK_EINVAL, "negative batch");
   if (batch == 0) return HK_OK;
   if (!alpha) return fail(HK_EINVAL, "alpha is NULL");
+  if (!xs) return fail(HK_EINVAL, "xs is NULL");
+  const int single = check_single(plan, h, xs, nx);
+  if (single < 0) return single;
   if (plan->two_level) return tl_run(plan, h, xs, nx, 0, batch, alpha, 1, workspace, stream, 1);
   Args1D a = base_args(plan, batch);
   if ((rc = set_h(plan, h, a))) return rc;
@@ -938,7 +1010,7 @@ int hk_tvp_full(const hk_plan *plan, hk_operand h, const hk_operand *xs, int nx,
   a.mode = hk::M_FULL;
   a.out = alpha;
   a.out_bstride = 1;
-  return launch(plan, a, stream);
+  return single ? launch_single(plan, a, stream) : launch(plan, a, stream);
 }
 
 int hk_vector_spectra(const hk_plan *plan, int mode, const void *mats, int64_t mat_stride,
@@ -999,6 +1071,7 @@ int hk_times_matrices(const hk_plan *plan, hk_operand h, const void *const *mats
   }
   if (batch == 0) return HK_OK;
   if (!T || !workspace) return fail(HK_EINVAL, "NULL output or workspace");
+  if (single_kind(h.dtype)) return fail(HK_EUNSUPPORTED, "times_matrices is complex128 only");
   if (plan->two_level)
     return tl_times_matrices(plan, h, mats, mat_strides, ranks, nmats, batch, T, t_stride,
                              workspace, stream, ncombo);

@@ -29,6 +29,21 @@ template <int N, class F>
 __device__ __forceinline__ void sfor(F &&f) { sfor_impl<0, N>(f); }
 
 // ---------------------------------------------------------------- complex helpers
+// Every codelet is generic over the complex type C: double2 (complex128, the
+// reference's precision) or float2 (the complex64 variant).
+template <class C>
+struct CT;
+template <>
+struct CT<double2> {
+  using S = double;
+  __device__ __forceinline__ static double2 make(double x, double y) { return make_double2(x, y); }
+};
+template <>
+struct CT<float2> {
+  using S = float;
+  __device__ __forceinline__ static float2 make(float x, float y) { return make_float2(x, y); }
+};
+
 __device__ __forceinline__ cplx cadd(cplx a, cplx b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ cplx csub(cplx a, cplx b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ cplx cmul(cplx a, cplx b) {
@@ -42,8 +57,21 @@ __device__ __forceinline__ cplx cscale(cplx a, double s) { return make_double2(a
 // a * (-i) and a * (+i)
 __device__ __forceinline__ cplx mul_mi(cplx a) { return make_double2(a.y, -a.x); }
 __device__ __forceinline__ cplx mul_pi(cplx a) { return make_double2(-a.y, a.x); }
-template <bool INV>
-__device__ __forceinline__ cplx cmul_dir(cplx a, cplx w) { return INV ? cmulc(a, w) : cmul(a, w); }
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }
+__device__ __forceinline__ float2 mul_pi(float2 a) { return make_float2(-a.y, a.x); }
+
+template <bool INV, class C>
+__device__ __forceinline__ C cmul_dir(C a, C w) { return INV ? cmulc(a, w) : cmul(a, w); }
 
 // ---------------------------------------------------------------- constexpr twiddles
 // cos / sin of 2*pi*e/R computed at compile time: exact integer reduction to a
@@ -97,21 +125,22 @@ constexpr double tw_sin(long long e, long long R) {
 }
 
 // a * exp(sign * 2*pi*i*E/R), sign = -1 forward, +1 inverse; E, R compile time.
-template <int E, int R, bool INV>
-__device__ __forceinline__ cplx twc(cplx a) {
+template <int E, int R, bool INV, class C>
+__device__ __forceinline__ C twc(C a) {
+  using S = typename CT<C>::S;
   constexpr int e = ((E % R) + R) % R;
   if constexpr (e == 0) {
     return a;
   } else if constexpr (4 * e == 2 * R) {
-    return make_double2(-a.x, -a.y);
+    return CT<C>::make(-a.x, -a.y);
   } else if constexpr (4 * e == R) {
     return INV ? mul_pi(a) : mul_mi(a);
   } else if constexpr (4 * e == 3 * R) {
     return INV ? mul_mi(a) : mul_pi(a);
   } else {
-    constexpr double c = tw_cos(e, R);
-    constexpr double s = INV ? tw_sin(e, R) : -tw_sin(e, R);
-    return make_double2(fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c));
+    constexpr S c = (S)tw_cos(e, R);
+    constexpr S s = (S)(INV ? tw_sin(e, R) : -tw_sin(e, R));
+    return CT<C>::make(fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c));
   }
 }
 
@@ -121,13 +150,15 @@ struct Dft;
 
 template <bool INV>
 struct Dft<1, INV> {
-  __device__ __forceinline__ static void run(cplx *) {}
+  template <class C>
+  __device__ __forceinline__ static void run(C *) {}
 };
 
 template <bool INV>
 struct Dft<2, INV> {
-  __device__ __forceinline__ static void run(cplx *v) {
-    cplx a = v[0], b = v[1];
+  template <class C>
+  __device__ __forceinline__ static void run(C *v) {
+    C a = v[0], b = v[1];
     v[0] = cadd(a, b);
     v[1] = csub(a, b);
   }
@@ -135,12 +166,14 @@ struct Dft<2, INV> {
 
 template <bool INV>
 struct Dft<3, INV> {
-  __device__ __forceinline__ static void run(cplx *v) {
-    constexpr double s3 = 0.866025403784438646763723170752936183;  // sin(2pi/3)
-    cplx a = v[0], s = cadd(v[1], v[2]), d = csub(v[1], v[2]);
-    cplx m = make_double2(fma(-0.5, s.x, a.x), fma(-0.5, s.y, a.y));
+  template <class C>
+  __device__ __forceinline__ static void run(C *v) {
+    using S = typename CT<C>::S;
+    constexpr S s3 = (S)0.866025403784438646763723170752936183;  // sin(2pi/3)
+    C a = v[0], s = cadd(v[1], v[2]), d = csub(v[1], v[2]);
+    C m = CT<C>::make(fma((S)-0.5, s.x, a.x), fma((S)-0.5, s.y, a.y));
     // forward: X1 = m - i*s3*d, X2 = m + i*s3*d
-    cplx r = make_double2(-s3 * d.y, s3 * d.x);  // i*s3*d
+    C r = CT<C>::make(-s3 * d.y, s3 * d.x);  // i*s3*d
     v[0] = cadd(a, s);
     if (INV) {
       v[1] = cadd(m, r);
@@ -154,9 +187,10 @@ struct Dft<3, INV> {
 
 template <bool INV>
 struct Dft<4, INV> {
-  __device__ __forceinline__ static void run(cplx *v) {
-    cplx t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
-    cplx t2 = cadd(v[1], v[3]), t3 = csub(v[1], v[3]);
+  template <class C>
+  __device__ __forceinline__ static void run(C *v) {
+    C t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+    C t2 = cadd(v[1], v[3]), t3 = csub(v[1], v[3]);
     t3 = INV ? mul_pi(t3) : mul_mi(t3);
     v[0] = cadd(t0, t2);
     v[2] = csub(t0, t2);
@@ -175,11 +209,12 @@ struct Dft {
   static constexpr int R1 = first_factor(R);
   static constexpr int R2 = R / R1;
   static_assert(R1 * R2 == R, "radix must factor into 2,3,4");
-  __device__ __forceinline__ static void run(cplx *v) {
-    cplx t[R];
+  template <class C>
+  __device__ __forceinline__ static void run(C *v) {
+    C t[R];
     sfor<R2>([&](auto n2c) {
       constexpr int n2 = decltype(n2c)::value;
-      cplx a[R1];
+      C a[R1];
       sfor<R1>([&](auto n1c) {
         constexpr int n1 = decltype(n1c)::value;
         a[n1] = v[n1 * R2 + n2];
@@ -192,7 +227,7 @@ struct Dft {
     });
     sfor<R1>([&](auto k1c) {
       constexpr int k1 = decltype(k1c)::value;
-      cplx b[R2];
+      C b[R2];
       sfor<R2>([&](auto n2c) {
         constexpr int n2 = decltype(n2c)::value;
         b[n2] = t[k1 * R2 + n2];
@@ -209,9 +244,10 @@ struct Dft {
 // radix-8 as 2 x 4 keeps the W8 twiddles to the two odd slots
 template <bool INV>
 struct Dft<8, INV> {
-  __device__ __forceinline__ static void run(cplx *v) {
-    cplx e[4] = {v[0], v[2], v[4], v[6]};
-    cplx o[4] = {v[1], v[3], v[5], v[7]};
+  template <class C>
+  __device__ __forceinline__ static void run(C *v) {
+    C e[4] = {v[0], v[2], v[4], v[6]};
+    C o[4] = {v[1], v[3], v[5], v[7]};
     Dft<4, INV>::run(e);
     Dft<4, INV>::run(o);
     o[1] = twc<1, 8, INV>(o[1]);
@@ -240,7 +276,8 @@ struct DftP;
 // small radices: full codelet when nothing is pruned, direct sums otherwise
 template <int R, bool INV, int NZ, int NO>
 struct DftP<R, INV, NZ, NO, false> {
-  __device__ __forceinline__ static void run(cplx *v) {
+  template <class C>
+  __device__ __forceinline__ static void run(C *v) {
     if constexpr (NZ >= R && NO >= R) {
       Dft<R, INV>::run(v);
     } else if constexpr (NZ == 1) {
@@ -249,11 +286,11 @@ struct DftP<R, INV, NZ, NO, false> {
         if constexpr (k > 0) v[k] = v[0];
       });
     } else {
-      cplx x[NZ];
+      C x[NZ];
       sfor<NZ>([&](auto nc) { x[decltype(nc)::value] = v[decltype(nc)::value]; });
       sfor<NO>([&](auto kc) {
         constexpr int k = decltype(kc)::value;
-        cplx s = x[0];
+        C s = x[0];
         sfor<NZ - 1>([&](auto nc) {
           constexpr int n = decltype(nc)::value + 1;
           s = cadd(s, twc<n * k, R, INV>(x[n]));
@@ -270,16 +307,17 @@ struct DftP<R, INV, NZ, NO, true> {
   static constexpr int R2 = R / R1;
   static constexpr int NZ2 = NZ < R2 ? NZ : R2;  // nonzero n2 columns
   static constexpr int NO1 = NO < R1 ? NO : R1;  // needed k1 rows
-  __device__ __forceinline__ static void run(cplx *v) {
+  template <class C>
+  __device__ __forceinline__ static void run(C *v) {
     if constexpr (NZ >= R && NO >= R) {
       Dft<R, INV>::run(v);
     } else {
-      cplx t[R];
+      C t[R];
       sfor<NZ2>([&](auto n2c) {
         constexpr int n2 = decltype(n2c)::value;
         constexpr int nz1c = (NZ - n2 + R2 - 1) / R2;
         constexpr int nz1 = nz1c > R1 ? R1 : nz1c;
-        cplx a[R1];
+        C a[R1];
         sfor<nz1>([&](auto n1c) {
           constexpr int n1 = decltype(n1c)::value;
           a[n1] = v[n1 * R2 + n2];
@@ -294,7 +332,7 @@ struct DftP<R, INV, NZ, NO, true> {
         constexpr int k1 = decltype(k1c)::value;
         constexpr int no2c = (NO - k1 + R1 - 1) / R1;
         constexpr int no2 = no2c > R2 ? R2 : no2c;
-        cplx b[R2];
+        C b[R2];
         sfor<NZ2>([&](auto n2c) {
           constexpr int n2 = decltype(n2c)::value;
           b[n2] = t[k1 * R2 + n2];

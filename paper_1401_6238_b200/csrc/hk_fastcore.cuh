@@ -13,6 +13,17 @@ namespace hk {
 namespace fast {
 
 __device__ __forceinline__ int swz2(int pos) { return pos ^ (((pos >> 4) ^ (pos >> 8)) & 7); }
+// 8-byte (complex64) elements are served 16 lanes per wavefront: XOR the low
+// FOUR position bits with bits 4-7 ^ 8-11 (conflict-free in every pass of the
+// radix-16 plans for both thread mappings used by `pass`).
+__device__ __forceinline__ int swz8(int pos) { return pos ^ (((pos >> 4) ^ (pos >> 8)) & 15); }
+template <class C>
+__device__ __forceinline__ int swzc(int pos) {
+  if constexpr (sizeof(C) == 8)
+    return swz8(pos);
+  else
+    return swz2(pos);
+}
 
 // Cheap addressing of swz2-swizzled shared memory for radix-16 plans with
 // L <= 4096 (positions = 3 hex digits d2 d1 d0).  In the pass over hex digit q
@@ -108,15 +119,21 @@ struct ChunkOf<T, std::void_t<decltype(T::kChunk)>> {
 // Pass-0 twiddles by recurrence: W_L^{j beta} = (W_L^beta)^j from one table
 // read per butterfly (two interleaved chains, <= 8 products deep), trading
 // 14 complex multiplies for 15 table reads (TMEM or L1 traffic).
-struct Tw0Rec {
-  const cplx *__restrict__ tw;  // W_L^e, e in [0, L)
-  __device__ __forceinline__ cplx base(int beta) const { return __ldg(&tw[beta]); }
+template <class C>
+struct Tw0RecT {
+  const C *__restrict__ tw;  // W_L^e, e in [0, L)
+  __device__ __forceinline__ C base(int beta) const { return __ldg(&tw[beta]); }
 };
+using Tw0Rec = Tw0RecT<cplx>;
+template <class T>
+struct is_tw0rec : std::false_type {};
+template <class C>
+struct is_tw0rec<Tw0RecT<C>> : std::true_type {};
 
-template <int R, bool INV>
-__device__ __forceinline__ void twiddle_rec(cplx (&a)[R], cplx w1) {
-  const cplx w2 = cmul(w1, w1);
-  cplx wo = w1, we = w2;
+template <int R, bool INV, class C>
+__device__ __forceinline__ void twiddle_rec(C (&a)[R], C w1) {
+  const C w2 = cmul(w1, w1);
+  C wo = w1, we = w2;
 #pragma unroll
   for (int j = 1; j < R; j += 2) {
     a[j] = cmul_dir<INV>(a[j], wo);
@@ -149,8 +166,8 @@ struct Tw0Global {
 // shared-memory carve-out (the strided reads of a W_L table touch one 128-B
 // line per twiddle).
 template <class PL, int p, bool INV, bool FINAL, int NZ, int NO, int TWL = PL::L, bool REC = false,
-          class TW0, class Load, class Store>
-__device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const TW0 &tw0,
+          class TW0, class Load, class Store, class C>
+__device__ __forceinline__ void pass(int t, const C *__restrict__ tw, const TW0 &tw0,
                                      Load &&load, Store &&store) {
   using Tr = Traits<PL>;
   constexpr int R = PL::radix[p];
@@ -165,8 +182,8 @@ __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const T
   // Pass-0 recurrence bases of a thread's NB butterflies, beta = t + i*T:
   // W_L^beta = W_L^t * W_L^{i T}, the second factor a compile-time constant,
   // so one table read serves all NB butterflies (8192 = 2 x 16^3: NB = 8).
-  [[maybe_unused]] cplx base0 = make_double2(1.0, 0.0);
-  if constexpr (p == 0 && PL::P > 1 && NB > 1 && std::is_same_v<TW0, Tw0Rec>) base0 = tw0.base(t);
+  [[maybe_unused]] C base0 = CT<C>::make(1, 0);
+  if constexpr (p == 0 && PL::P > 1 && NB > 1 && is_tw0rec<TW0>::value) base0 = tw0.base(t);
 #pragma unroll
   for (int i = 0; i < NB; ++i) {
     const int beta = t + i * PL::T;
@@ -181,7 +198,7 @@ __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const T
       }
       const int base = hi * Lp + lo;
       constexpr int Q = PL::P - 1 - p;
-      cplx a[R];
+      C a[R];
       if constexpr (std::is_same_v<std::decay_t<Load>, SmemIO>) {
         const HexAddr<Q> ad(load.sbase, base);
         sfor<NIN>([&](auto jc) {
@@ -195,9 +212,9 @@ __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const T
         });
       }
       auto twiddle = [&]() {
-        if constexpr (p == 0 && PL::P > 1 && std::is_same_v<TW0, Tw0Rec>) {
+        if constexpr (p == 0 && PL::P > 1 && is_tw0rec<TW0>::value) {
           if constexpr (NB > 1) {
-            cplx bi = base0;
+            C bi = base0;
             sfor<NB>([&](auto ic) {  // constant index: bi = base0 * W_L^{i T}
               constexpr int ii = decltype(ic)::value;
               if (ii == i) bi = twc<ii * PL::T, PL::L, false>(base0);
@@ -211,7 +228,7 @@ __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const T
           constexpr int CK = ChunkOf<TW0>::value;
           sfor<(R - 1 + CK - 1) / CK>([&](auto cc) {
             constexpr int c = decltype(cc)::value;
-            cplx w[CK];
+            C w[CK];
             tw0.chunk(beta, c, w);
             sfor<CK>([&](auto qc) {
               constexpr int j = CK * c + decltype(qc)::value + 1;
@@ -226,7 +243,7 @@ __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const T
           sfor<(R - 1 + 3) / 4>([&](auto cc) {
             constexpr int c = decltype(cc)::value;
             asm volatile("" ::: "memory");
-            cplx w[4];
+            C w[4];
             sfor<4>([&](auto qc) {
               constexpr int j = 4 * c + decltype(qc)::value + 1;
               if constexpr (j < R) w[decltype(qc)::value] = __ldg(&tw[j * lo * (TWL / Lp)]);
@@ -261,9 +278,9 @@ __device__ __forceinline__ void pass(int t, const cplx *__restrict__ tw, const T
   }
 }
 
-template <class PL, class Lambda>
+template <class PL, class C, class Lambda>
 __device__ __forceinline__ decltype(auto) pick_io(Lambda &l, const SmemIO &sio) {
-  if constexpr (hex_plan<PL>())
+  if constexpr (hex_plan<PL>() && sizeof(C) == 16)
     return (sio);
   else
     return (l);
@@ -295,9 +312,9 @@ struct NoHook {
 // hook() runs (on every thread) right after the barrier that follows pass 0,
 // i.e. once every thread of the group has consumed the pass-0 input.
 template <class PL, bool INV, int NZ, int TWL = PL::L, bool REC = false, class TW0, class GLoad,
-          class Sync = CtaSync, class Hook = NoHook>
-__device__ __forceinline__ void fft_dif(cplx *sbuf, int t, const cplx *__restrict__ tw,
-                                        const TW0 &tw0, GLoad &&gload, cplx (&out)[PL::V],
+          class Sync = CtaSync, class Hook = NoHook, class C>
+__device__ __forceinline__ void fft_dif(C *sbuf, int t, const C *__restrict__ tw,
+                                        const TW0 &tw0, GLoad &&gload, C (&out)[PL::V],
                                         Sync sync = Sync(), Hook hook = Hook()) {
   constexpr int RL = PL::Rlast;
   constexpr int R0 = PL::radix[0];
@@ -308,12 +325,12 @@ __device__ __forceinline__ void fft_dif(cplx *sbuf, int t, const cplx *__restric
     else
       return gload(pos);
   };
-  auto s_load_l = [&](int, int, int pos) { return sbuf[swz2(pos)]; };
-  auto s_store_l = [&](int, int, int pos, cplx v) { sbuf[swz2(pos)] = v; };
-  auto r_store = [&](int i, int j, int, cplx v) { out[i * RL + j] = v; };
+  auto s_load_l = [&](int, int, int pos) { return sbuf[swzc<C>(pos)]; };
+  auto s_store_l = [&](int, int, int pos, C v) { sbuf[swzc<C>(pos)] = v; };
+  auto r_store = [&](int i, int j, int, C v) { out[i * RL + j] = v; };
   const SmemIO sio{smem_u32(sbuf)};
-  auto &&s_load = pick_io<PL>(s_load_l, sio);
-  auto &&s_store = pick_io<PL>(s_store_l, sio);
+  auto &&s_load = pick_io<PL, C>(s_load_l, sio);
+  auto &&s_store = pick_io<PL, C>(s_store_l, sio);
   static_assert(PL::P >= 2, "fast path needs at least two passes");
   sync();
   using SL = decltype(s_load);
@@ -334,19 +351,19 @@ __device__ __forceinline__ void fft_dif(cplx *sbuf, int t, const cplx *__restric
 }
 
 template <class PL, int NO, int TWL = PL::L, bool REC = false, class TW0, class GStore,
-          class Sync = CtaSync>
-__device__ __forceinline__ void fft_final(cplx *sbuf, int t, const cplx *__restrict__ tw,
-                                          const TW0 &tw0, cplx (&in)[PL::V], GStore &&gstore,
+          class Sync = CtaSync, class C>
+__device__ __forceinline__ void fft_final(C *sbuf, int t, const C *__restrict__ tw,
+                                          const TW0 &tw0, C (&in)[PL::V], GStore &&gstore,
                                           Sync sync = Sync()) {
   constexpr int RL = PL::Rlast;
   constexpr int R0 = PL::radix[0];
   auto r_load = [&](int i, int j, int) { return in[i * RL + j]; };
-  auto s_load_l = [&](int, int, int pos) { return sbuf[swz2(pos)]; };
-  auto s_store_l = [&](int, int, int pos, cplx v) { sbuf[swz2(pos)] = v; };
-  auto g_store = [&](int, int, int pos, cplx v) { gstore(pos, v); };
+  auto s_load_l = [&](int, int, int pos) { return sbuf[swzc<C>(pos)]; };
+  auto s_store_l = [&](int, int, int pos, C v) { sbuf[swzc<C>(pos)] = v; };
+  auto g_store = [&](int, int, int pos, C v) { gstore(pos, v); };
   const SmemIO sio{smem_u32(sbuf)};
-  auto &&s_load = pick_io<PL>(s_load_l, sio);
-  auto &&s_store = pick_io<PL>(s_store_l, sio);
+  auto &&s_load = pick_io<PL, C>(s_load_l, sio);
+  auto &&s_store = pick_io<PL, C>(s_store_l, sio);
   sync();
   using SL = decltype(s_load);
   using SS = decltype(s_store);
@@ -376,6 +393,16 @@ __device__ __forceinline__ cplx ld_stream(const cplx *p) {
   asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
+__device__ __forceinline__ float ld_stream(const float *p) {
+  float v;
+  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];\n" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float2 ld_stream(const float2 *p) {
+  float2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];\n" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
 
 // Per-thread asynchronous copies (LDGSTS) with zero fill past the operand end.
 __device__ __forceinline__ void cpa16(uint32_t dst, const void *src, bool ok) {
@@ -401,6 +428,20 @@ __device__ __forceinline__ cplx load_elem(const Factor &f, long long off, int po
   const cplx *p = static_cast<const cplx *>(f.ptr) + off;
   cplx v = ld_stream(p + k);
   return make_double2(v.x * scale, v.y * scale);
+}
+
+// complex64 variant: FK_C64 / FK_F32 operands.
+__device__ __forceinline__ float2 load_elem_f(const Factor &f, long long off, int pos,
+                                              float scale) {
+  if (pos >= f.len) return make_float2(0.f, 0.f);
+  const long long k = (long long)pos * f.estride;
+  if (f.kind == FK_F32) {
+    const float *p = static_cast<const float *>(f.ptr) + off;
+    return make_float2(ld_stream(p + k) * scale, 0.f);
+  }
+  const float2 *p = static_cast<const float2 *>(f.ptr) + off;
+  const float2 v = ld_stream(p + k);
+  return make_float2(v.x * scale, v.y * scale);
 }
 
 }  // namespace fast

@@ -59,11 +59,49 @@ struct Plan1D {
   static constexpr int SMEM_BYTES = (P > 1) ? G * L * (int)sizeof(cplx) : 16;
 };
 
+// Supported on-chip lengths.  Power-of-two lengths use radix-16 passes with one
+// small leading radix; 3*2^k lengths put a radix-12/24/3/6 pass first.
+#define HK_PLAN_LIST(X)                     \
+  X(2, Plan1D<2, 1, 2>)                     \
+  X(4, Plan1D<4, 1, 4>)                     \
+  X(8, Plan1D<8, 1, 8>)                     \
+  X(16, Plan1D<16, 1, 16>)                  \
+  X(32, Plan1D<32, 2, 2, 16>)               \
+  X(64, Plan1D<64, 4, 4, 16>)               \
+  X(128, Plan1D<128, 8, 8, 16>)             \
+  X(256, Plan1D<256, 16, 16, 16>)           \
+  X(512, Plan1D<512, 32, 2, 16, 16>)        \
+  X(1024, Plan1D<1024, 64, 4, 16, 16>)      \
+  X(2048, Plan1D<2048, 128, 8, 16, 16>)     \
+  X(4096, Plan1D<4096, 256, 16, 16, 16>)    \
+  X(8192, Plan1D<8192, 512, 2, 16, 16, 16>) \
+  X(12, Plan1D<12, 1, 12>)                  \
+  X(24, Plan1D<24, 1, 24>)                  \
+  X(48, Plan1D<48, 3, 3, 16>)               \
+  X(96, Plan1D<96, 6, 6, 16>)               \
+  X(192, Plan1D<192, 12, 12, 16>)           \
+  X(384, Plan1D<384, 24, 24, 16>)           \
+  X(768, Plan1D<768, 48, 3, 16, 16>)        \
+  X(1536, Plan1D<1536, 96, 6, 16, 16>)      \
+  X(3072, Plan1D<3072, 192, 12, 16, 16>)    \
+  X(6144, Plan1D<6144, 384, 24, 16, 16>)
+
 __device__ __forceinline__ int swz(int pos) { return pos ^ ((pos >> 4) & 7); }
+// Swizzle by element size: 16-byte (complex128) elements as above; 8-byte
+// (complex64) elements are served 16 lanes per phase, so the low 4 position
+// bits are XORed with bits 4-7 (the last radix-16 pass reads 16 consecutive
+// positions per thread at a 16-element lane stride).
+template <class C>
+__device__ __forceinline__ int swz_t(int pos) {
+  if constexpr (sizeof(C) == 8)
+    return pos ^ ((pos >> 4) & 15);
+  else
+    return swz(pos);
+}
 
 // One DIF pass.  load(pos) -> cplx ; store(i, j, pos, value).
-template <class PL, int p, bool INV, class Load, class Store>
-__device__ __forceinline__ void dif_pass(int t, const cplx *__restrict__ tw, Load &&load,
+template <class PL, int p, bool INV, class C, class Load, class Store>
+__device__ __forceinline__ void dif_pass(int t, const C *__restrict__ tw, Load &&load,
                                          Store &&store) {
   constexpr int R = PL::radix[p];
   constexpr int s = PL::stride(p);
@@ -76,7 +114,7 @@ __device__ __forceinline__ void dif_pass(int t, const cplx *__restrict__ tw, Loa
     if (NBUT % PL::T == 0 || beta < NBUT) {
       const int lo = beta % s;
       const int base = (beta / s) * Lp + lo;
-      cplx a[R];
+      C a[R];
       sfor<R>([&](auto jc) {
         constexpr int j = decltype(jc)::value;
         a[j] = load(base + j * s);
@@ -99,8 +137,8 @@ __device__ __forceinline__ void dif_pass(int t, const cplx *__restrict__ tw, Loa
 
 // One transposed (DIT) pass of the forward transform: twiddle, then butterfly.
 // load(i, j, pos) -> cplx ; store(i, j, pos, value).
-template <class PL, int p, class Load, class Store>
-__device__ __forceinline__ void dit_pass(int t, const cplx *__restrict__ tw, Load &&load,
+template <class PL, int p, class C, class Load, class Store>
+__device__ __forceinline__ void dit_pass(int t, const C *__restrict__ tw, Load &&load,
                                          Store &&store) {
   constexpr int R = PL::radix[p];
   constexpr int s = PL::stride(p);
@@ -113,7 +151,7 @@ __device__ __forceinline__ void dit_pass(int t, const cplx *__restrict__ tw, Loa
     if (NBUT % PL::T == 0 || beta < NBUT) {
       const int lo = beta % s;
       const int base = (beta / s) * Lp + lo;
-      cplx a[R];
+      C a[R];
       sfor<R>([&](auto jc) {
         constexpr int j = decltype(jc)::value;
         a[j] = load(i, j, base + j * s);
@@ -135,16 +173,16 @@ __device__ __forceinline__ void dit_pass(int t, const cplx *__restrict__ tw, Loa
 }
 
 // Full DIF transform: global loader -> registers (digit-reversed).
-template <class PL, bool INV, class GLoad>
-__device__ __forceinline__ void fft_dif(cplx *sbuf, int t, const cplx *__restrict__ tw,
-                                        GLoad &&gload, cplx (&out)[PL::V]) {
+template <class PL, bool INV, class C, class GLoad>
+__device__ __forceinline__ void fft_dif(C *sbuf, int t, const C *__restrict__ tw,
+                                        GLoad &&gload, C (&out)[PL::V]) {
   constexpr int RL = PL::Rlast;
-  auto reg_store = [&](int i, int j, int, cplx v) { out[i * RL + j] = v; };
+  auto reg_store = [&](int i, int j, int, C v) { out[i * RL + j] = v; };
   if constexpr (PL::P == 1) {
     dif_pass<PL, 0, INV>(t, tw, gload, reg_store);
   } else {
-    auto s_load = [&](int pos) { return sbuf[swz(pos)]; };
-    auto s_store = [&](int, int, int pos, cplx v) { sbuf[swz(pos)] = v; };
+    auto s_load = [&](int pos) { return sbuf[swz_t<C>(pos)]; };
+    auto s_store = [&](int, int, int pos, C v) { sbuf[swz_t<C>(pos)] = v; };
     __syncthreads();  // previous readers of sbuf are done
     dif_pass<PL, 0, INV>(t, tw, gload, s_store);
     sfor<PL::P - 2>([&](auto qc) {
@@ -158,17 +196,17 @@ __device__ __forceinline__ void fft_dif(cplx *sbuf, int t, const cplx *__restric
 }
 
 // Final forward transform: digit-reversed registers -> natural order via gstore(pos, v).
-template <class PL, class GStore>
-__device__ __forceinline__ void fft_dit_final(cplx *sbuf, int t, const cplx *__restrict__ tw,
-                                              cplx (&in)[PL::V], GStore &&gstore) {
+template <class PL, class C, class GStore>
+__device__ __forceinline__ void fft_dit_final(C *sbuf, int t, const C *__restrict__ tw,
+                                              C (&in)[PL::V], GStore &&gstore) {
   constexpr int RL = PL::Rlast;
   auto reg_load = [&](int i, int j, int) { return in[i * RL + j]; };
-  auto g_store = [&](int, int, int pos, cplx v) { gstore(pos, v); };
+  auto g_store = [&](int, int, int pos, C v) { gstore(pos, v); };
   if constexpr (PL::P == 1) {
     dit_pass<PL, 0>(t, tw, reg_load, g_store);
   } else {
-    auto s_load = [&](int, int, int pos) { return sbuf[swz(pos)]; };
-    auto s_store = [&](int, int, int pos, cplx v) { sbuf[swz(pos)] = v; };
+    auto s_load = [&](int, int, int pos) { return sbuf[swz_t<C>(pos)]; };
+    auto s_store = [&](int, int, int pos, C v) { sbuf[swz_t<C>(pos)] = v; };
     __syncthreads();
     dit_pass<PL, PL::P - 1>(t, tw, reg_load, s_store);
     sfor<PL::P - 2>([&](auto qc) {

@@ -11,6 +11,8 @@ enum FactorKind : int32_t {
   FK_C128 = 0,  // complex128 vector, zero-padded to L and transformed in-kernel
   FK_F64 = 1,   // float64 vector (imaginary part zero), zero-padded and transformed
   FK_SPEC = 2,  // precomputed spectrum in the kernel's internal layout (length L)
+  FK_C64 = 3,   // complex64 vector (complex64 variant, hk_c64.cu)
+  FK_F32 = 4,   // float32 vector (complex64 variant)
 };
 
 enum Mode1D : int32_t {
@@ -52,6 +54,7 @@ struct Args1D {
   const double2 *tw;        // W_L^e, e in [0, L)
   const double2 *tw0;       // thread-major first-pass table (fast path), may be NULL
   const double2 *tw1;       // W_{L/R0}^e, e in [0, L/R0): passes >= 1 of the fast path, may be NULL
+  const float2 *twf;        // complex64 variant: W_L^e in single precision
   double scale;             // 1/L for the inverse transform
   int32_t prefetch;         // fast path: L2-prefetch the next block's operands
   // times_matrices combo table (ncombo > 0): launch item q = b * ncombo + c;
@@ -73,6 +76,8 @@ cudaError_t launch_fast_1d(int L, const Args1D &a, cudaStream_t stream);
 int fast_first_radix(long long L);  // R_0 of the fast plan, 0 if none
 // Producer/consumer TMA variant (hk_pp1d.cu) for batched H x^{m-1}.
 cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream);
+// complex64 / float32 variant (hk_c64.cu): M_PARTIAL and M_FULL, on-chip L.
+cudaError_t launch_c64_1d(int L, const Args1D &a, cudaStream_t stream);
 // Latency kernel (hk_small.cu) for a few small direct products.
 cudaError_t launch_small_1d(int L, const Args1D &a, cudaStream_t stream);
 

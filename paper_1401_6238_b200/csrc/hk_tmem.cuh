@@ -105,3 +105,29 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, cplx *v) {
 }
 
 }  // namespace hk
+
+namespace hk {
+
+// 4 complex floats = 8 consecutive 32-bit columns (complex64 variant).
+__device__ __forceinline__ void tmem_st4f(uint32_t taddr, const float2 *v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::
+                   "r"(taddr),
+               "r"(__float_as_uint(v[0].x)), "r"(__float_as_uint(v[0].y)),
+               "r"(__float_as_uint(v[1].x)), "r"(__float_as_uint(v[1].y)),
+               "r"(__float_as_uint(v[2].x)), "r"(__float_as_uint(v[2].y)),
+               "r"(__float_as_uint(v[3].x)), "r"(__float_as_uint(v[3].y)));
+}
+
+__device__ __forceinline__ void tmem_ld4f(uint32_t taddr, float2 *v) {
+  uint32_t r[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+      "tcgen05.wait::ld.sync.aligned;\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+}
+
+}  // namespace hk

@@ -46,11 +46,12 @@ def leading_left_singular(M: torch.Tensor, r: int) -> torch.Tensor:
     leading part of the spectrum, so squaring the condition number costs
     ~eps*sigma_1^2/gap^2 (measured 2e-13 on cfg5 against the SVD) while the
     batched library SVD of 256 x (2000 x 25) is ~500x slower.  The shortcut is
-    only trusted when it is well posed: items whose r-th eigenvalue gap is
-    below 1e-5 sigma_1^2, whose r-th singular value vanishes, or whose factor
-    is not orthonormal to 1e-12 (rank-deficient or ill-conditioned M) are
-    recomputed with the SVD, which always returns orthonormal factors like
-    the reference.  Other shapes use the SVD directly.
+    only trusted when it is well posed: one Cholesky-QR pass re-orthonormalises
+    the factor inside its span, and items whose r-th eigenvalue gap is below
+    1e-5 sigma_1^2, whose r-th singular value vanishes, or whose factor is
+    still not orthonormal to 1e-12 (rank-deficient or ill-conditioned M) are
+    recomputed with the SVD, which always returns orthonormal factors like the
+    reference.  Other shapes use the SVD directly.
     """
     rows, cols = M.shape[-2], M.shape[-1]
     if not 1 <= r <= min(rows, cols):
@@ -69,6 +70,15 @@ def leading_left_singular(M: torch.Tensor, r: int) -> torch.Tensor:
         ok = (s[..., -1] > 0) & (gap >= 1e-5)
         s = torch.where(s > 0, s, torch.ones_like(s))
         U = (Mb @ Vr.to(Mb.dtype)) / s[..., None, :].to(Mb.dtype)
+        # one Cholesky-QR pass restores orthonormality lost to the squared
+        # condition number (~eps*kappa^2) without moving the span: U <- U L^-H
+        C = U.conj().transpose(-1, -2) @ U
+        Lc, info = torch.linalg.cholesky_ex(C)
+        ok &= info == 0
+        Lc = torch.where((info == 0)[..., None, None], Lc, torch.eye(r, dtype=C.dtype,
+                                                                    device=C.device))
+        U = torch.linalg.solve_triangular(Lc.conj().transpose(-1, -2), U, upper=True,
+                                          left=False)
         eye = torch.eye(r, dtype=U.dtype, device=U.device)
         ortho = (U.conj().transpose(-1, -2) @ U - eye).abs().amax(dim=(-2, -1))
         ok &= (ortho <= 1e-12) & torch.isfinite(ortho)

@@ -23,7 +23,7 @@ def _run(*extra):
 
 
 def test_ours_line_contract():
-    d = _run("--no-extras", "--ref-products-per-core", "16")
+    d = _run("--no-extras", "--cpu-quick")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
               "higher_is_better", "scaling", "vs_baseline", "dtype", "config", "roofline", "e2e",
               "gpu_launches", "clocks", "cpu_baseline"):
@@ -39,10 +39,14 @@ def test_ours_line_contract():
     assert d["gpu_launches"] == 3
     c = d["cpu_baseline"]
     assert c["kind"] in ("port", "reference") and c["cores"] >= 1 and c["value"] > 0
+    assert c["one_core"] > 0 and c["exact_all_cores"] > 0 and c["pow2_all_cores"] > 0
+    # the timed output itself matches the reference's own cfg2 outputs
+    assert d["parity_rel_err"] <= 1e-10 and d["parity_norms_checked"] == 4096
+    assert d["gather"]["ms"] >= 0
 
 
 def test_reference_line_contract():
-    d = _run("--impl", "reference", "--ref-products-per-core", "16")
+    d = _run("--impl", "reference")
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["value"] == d["value"]
