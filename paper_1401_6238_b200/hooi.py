@@ -40,18 +40,22 @@ def fix_phase_batched(U: torch.Tensor) -> torch.Tensor:
 def leading_left_singular(M: torch.Tensor, r: int) -> torch.Tensor:
     """truncated_left_singular_vectors (decompose.py:35-41), batched.
 
-    Tall-skinny M (the HOOI unfoldings, n x r^(m-1)) go through the Gram
-    matrix: G = M^H M (one batched GEMM), batched Hermitian eigh of the small
-    G, U = M V Sigma^{-1}.  Leading singular vectors only depend on the
-    leading part of the spectrum, so squaring the condition number costs
-    ~eps*sigma_1^2/gap^2 (measured 2e-13 on cfg5 against the SVD) while the
-    batched library SVD of 256 x (2000 x 25) is ~500x slower.  The shortcut is
-    only trusted when it is well posed: one Cholesky-QR pass re-orthonormalises
-    the factor inside its span, and items whose r-th eigenvalue gap is below
-    1e-5 sigma_1^2, whose r-th singular value vanishes, or whose factor is
-    still not orthonormal to 1e-12 (rank-deficient or ill-conditioned M) are
-    recomputed with the SVD, which always returns orthonormal factors like the
-    reference.  Other shapes use the SVD directly.
+    Tall-skinny M (the HOOI unfoldings, n x r^(m-1), e.g. 2000 x 25) go through
+    the Gram matrix: G = M^H M (one batched GEMM), the batched Hermitian
+    eigensolver on the small G (cuSOLVER's batched Jacobi, <= 32 x 32), and
+    U = M V Sigma^{-1}, then one Cholesky-QR pass U <- U chol(U^H U)^{-H} that
+    restores orthonormality inside the same span.  Squaring the condition
+    number perturbs the span by ~eps sigma_1^2 / (sigma_r^2 - sigma_{r+1}^2)
+    (measured 2e-13 on cfg5 against the SVD; the 50-sweep fixed point matches
+    the reference's own SVD loop to 3e-15, tests/test_gpu_r2_parity.py), while
+    the library SVD of 256 x (2000 x 25) -- or the Jacobi eigensolver on the
+    50 x 50 Jordan-Wielandt form, beyond the batched solver's 32 x 32 limit --
+    is 50-250x slower on the device.  Items that are numerically rank
+    deficient (sigma_r ~ 0, Cholesky failure, or a factor not orthonormal to
+    1e-12 -- the rank-1 all-ones tensor asked for r = 2) take a Householder QR
+    of M and the SVD of its small R instead, so factors are always orthonormal
+    like the reference's.  Other shapes use the library SVD directly.  Phases
+    as fix_phase (decompose.py:23-32).
     """
     rows, cols = M.shape[-2], M.shape[-1]
     if not 1 <= r <= min(rows, cols):
@@ -59,34 +63,27 @@ def leading_left_singular(M: torch.Tensor, r: int) -> torch.Tensor:
     if rows >= 2 * cols:
         batch_shape = M.shape[:-2]
         Mb = M.reshape(-1, rows, cols)
-        G = Mb.conj().transpose(-1, -2) @ Mb
+        G = Mb.mH @ Mb
         w, V = torch.linalg.eigh(G)                       # ascending
         Vr = V[..., -r:].flip(-1)
-        wr = w[..., -r:].flip(-1)
+        s = torch.sqrt(torch.clamp(w[..., -r:].flip(-1), min=0.0))
         w1 = w[..., -1].clamp(min=torch.finfo(w.dtype).tiny)
-        w_next = w[..., -r - 1] if r < cols else torch.zeros_like(w1)
-        gap = (w[..., -r] - w_next) / w1
-        s = torch.sqrt(torch.clamp(wr, min=0.0))
-        ok = (s[..., -1] > 0) & (gap >= 1e-5)
+        ok = s[..., -1] ** 2 > 1e-13 * w1
         s = torch.where(s > 0, s, torch.ones_like(s))
         U = (Mb @ Vr.to(Mb.dtype)) / s[..., None, :].to(Mb.dtype)
-        # one Cholesky-QR pass restores orthonormality lost to the squared
-        # condition number (~eps*kappa^2) without moving the span: U <- U L^-H
-        C = U.conj().transpose(-1, -2) @ U
-        Lc, info = torch.linalg.cholesky_ex(C)
-        ok &= info == 0
-        Lc = torch.where((info == 0)[..., None, None], Lc, torch.eye(r, dtype=C.dtype,
-                                                                    device=C.device))
-        U = torch.linalg.solve_triangular(Lc.conj().transpose(-1, -2), U, upper=True,
-                                          left=False)
         eye = torch.eye(r, dtype=U.dtype, device=U.device)
-        ortho = (U.conj().transpose(-1, -2) @ U - eye).abs().amax(dim=(-2, -1))
+        L, info = torch.linalg.cholesky_ex(U.mH @ U)
+        ok &= info == 0
+        L = torch.where((info == 0)[..., None, None], L, eye)
+        U = torch.linalg.solve_triangular(L.mH, U, upper=True, left=False)
+        ortho = (U.mH @ U - eye).abs().amax(dim=(-2, -1))
         ok &= (ortho <= 1e-12) & torch.isfinite(ortho)
         if not bool(ok.all()):
             bad = torch.nonzero(~ok).flatten()
-            Us, _, _ = torch.linalg.svd(Mb[bad], full_matrices=False)
+            Q, R = torch.linalg.qr(Mb[bad])
+            Ur, _, _ = torch.linalg.svd(R)
             U = U.clone()
-            U[bad] = Us[..., :r]
+            U[bad] = Q @ Ur[..., :r]
         return fix_phase_batched(U).reshape(*batch_shape, rows, r)
     U, _, _ = torch.linalg.svd(M, full_matrices=False)
     return fix_phase_batched(U[..., :r])
