@@ -13,6 +13,7 @@
 
 #include "hk_fft1d.cuh"
 #include "hk_internal.h"
+#include "hk_tmem.cuh"
 
 namespace hk {
 
@@ -34,38 +35,76 @@ __device__ __forceinline__ cplx load_factor(const Factor &f, long long off, int 
   return make_double2(v.x * scale, v.y * scale);
 }
 
+// The accumulator acc = ifft(h) .* prod X lives in TMEM (4 x 32-bit columns per
+// complex value, warp w on lanes 32*(w%4).. and slab w/4) whenever every
+// thread holds a multiple of 4 values, so only one length-L working set is in
+// registers while the next vector transform runs (with acc and w both in
+// registers the kernel needed 255 registers and still spilled 80-530 bytes).
+template <class PL>
+struct GenTr {
+  static constexpr bool tmem = PL::V % 4 == 0;
+  static constexpr int warps = PL::CTA / 32;
+  static constexpr int slabs = (warps + 3) / 4;
+  static constexpr int need = slabs * 4 * PL::V;
+  static constexpr int cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128
+                              : need <= 256 ? 256 : 512;
+  static_assert(!tmem || need <= 512, "accumulator does not fit in TMEM");
+};
+
 template <class PL>
 __global__ void __launch_bounds__(PL::CTA, 1) k_hankel_1d(const __grid_constant__ Args1D a) {
+  using Tr = GenTr<PL>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint32_t tmem_slot;
   cplx *smem = reinterpret_cast<cplx *>(smem_raw);
   constexpr int T = PL::T;
   constexpr int V = PL::V;
   const int g = threadIdx.x / T;
   const int t = threadIdx.x - g * T;
+  const int warp = threadIdx.x >> 5;
   long long b = (long long)blockIdx.x * PL::G + g;
   const bool active = b < a.batch;
   if (!active) b = a.batch - 1;  // idle groups shadow a valid item; their stores are masked
   const long long ob = b / a.nsub, os = b - (b / a.nsub) * a.nsub;
   cplx *sbuf = smem + (PL::P > 1 ? g * PL::L : 0);
   const cplx *__restrict__ tw = a.tw;
+  uint32_t tmy = 0;
+  if constexpr (Tr::tmem) {
+    if (warp == 0) tmem_alloc<Tr::cols>(&tmem_slot);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    tmy = tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 4 * V);
+  }
 
-  cplx acc[V];
+  cplx acc[Tr::tmem ? 1 : V];
+  cplx w[V];
+  auto acc_put = [&](cplx(&v)[V]) {
+    if constexpr (Tr::tmem) {
+#pragma unroll
+      for (int c = 0; c < V / 4; ++c) tmem_st4(tmy + 16 * c, &v[4 * c]);
+      tmem_wait_st();
+    } else {
+#pragma unroll
+      for (int r = 0; r < V; ++r) acc[r] = v[r];
+    }
+  };
   if (a.mode != M_SPEC_F) {
     if (a.h.kind == FK_SPEC) {
       const cplx *sp = static_cast<const cplx *>(a.h.ptr) + item_off(a.h.bstride, a.h.sstride, ob, os);
 #pragma unroll
-      for (int r = 0; r < V; ++r) acc[r] = __ldg(sp + r * T + t);
+      for (int r = 0; r < V; ++r) w[r] = __ldg(sp + r * T + t);
     } else {
       const Factor &hf = a.h;
       const double sc = a.scale;
       const long long off = item_off(hf.bstride, hf.sstride, ob, os);
-      fft_dif<PL, true>(sbuf, t, tw, [&](int pos) { return load_factor(hf, off, pos, sc); }, acc);
+      fft_dif<PL, true>(sbuf, t, tw, [&](int pos) { return load_factor(hf, off, pos, sc); }, w);
     }
+    acc_put(w);
   }
 
   for (int f = 0; f < a.nfac; ++f) {
     const Factor &fa = a.fac[f];
-    cplx w[V];
     const long long off =
         ob * fa.bstride + (a.ncombo ? (long long)a.combo_col[os][f] : os) * fa.sstride;
     if (fa.kind == FK_SPEC) {
@@ -76,14 +115,33 @@ __global__ void __launch_bounds__(PL::CTA, 1) k_hankel_1d(const __grid_constant_
       fft_dif<PL, false>(sbuf, t, tw, [&](int pos) { return load_factor(fa, off, pos, 1.0); }, w);
     }
     if (a.mode == M_SPEC_F) {
+      acc_put(w);
+    } else if constexpr (Tr::tmem) {
 #pragma unroll
-      for (int r = 0; r < V; ++r) acc[r] = w[r];
+      for (int c = 0; c < V / 4; ++c) {
+        cplx q[4];
+        tmem_ld4(tmy + 16 * c, q);
+        for (int k = 0; k < fa.power; ++k) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) q[e] = cmul(q[e], w[4 * c + e]);
+        }
+        tmem_st4(tmy + 16 * c, q);
+      }
+      tmem_wait_st();
     } else {
       for (int k = 0; k < fa.power; ++k) {
 #pragma unroll
         for (int r = 0; r < V; ++r) acc[r] = cmul(acc[r], w[r]);
       }
     }
+  }
+  // final: acc -> registers (w)
+  if constexpr (Tr::tmem) {
+#pragma unroll
+    for (int c = 0; c < V / 4; ++c) tmem_ld4(tmy + 16 * c, &w[4 * c]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < V; ++r) w[r] = acc[r];
   }
 
   cplx *out = static_cast<cplx *>(a.out) + ob * a.out_bstride +
@@ -94,7 +152,7 @@ __global__ void __launch_bounds__(PL::CTA, 1) k_hankel_1d(const __grid_constant_
   if (a.mode == M_PARTIAL) {
     const int n1 = a.out_len;
     const long long es = a.out_estride;
-    fft_dit_final<PL>(sbuf, t, tw, acc, [&](int pos, cplx v) {
+    fft_dit_final<PL>(sbuf, t, tw, w, [&](int pos, cplx v) {
       if (active && pos < n1) {
         out[pos * es] = v;
         if (out2) out2[pos * es] = v;
@@ -103,7 +161,7 @@ __global__ void __launch_bounds__(PL::CTA, 1) k_hankel_1d(const __grid_constant_
   } else if (a.mode == M_FULL) {
     cplx s = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int r = 0; r < V; ++r) s = cadd(s, acc[r]);
+    for (int r = 0; r < V; ++r) s = cadd(s, w[r]);
     // deterministic: per-thread partials in smem, summed in thread order
     __syncthreads();
     cplx *red = smem + g * T;  // G*T <= G*L slots
@@ -117,7 +175,15 @@ __global__ void __launch_bounds__(PL::CTA, 1) k_hankel_1d(const __grid_constant_
   } else {
     if (active) {
 #pragma unroll
-      for (int r = 0; r < V; ++r) out[r * T + t] = acc[r];
+      for (int r = 0; r < V; ++r) out[r * T + t] = w[r];
+    }
+  }
+  if constexpr (Tr::tmem) {
+    tmem_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+      tmem_fence_after();
+      tmem_dealloc<Tr::cols>(tmem_slot);
     }
   }
 }

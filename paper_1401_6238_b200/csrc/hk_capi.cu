@@ -245,6 +245,8 @@ int col_tables(int dev, long long L1, const double2 **tw, const double2 **tw0) {
     case 1024: r0 = 4; break;
     case 1536: r0 = 6; break;
     case 2048: r0 = 8; break;
+    case 3072: r0 = 12; break;
+    case 4096: r0 = 16; break;
     default: return fail(HK_EUNSUPPORTED, "no column plan of length %lld", L1);
   }
   int rc = get_twiddles(dev, L1, tw);
@@ -418,7 +420,7 @@ int hk_plan_create_hankel(hk_plan **plan, int order, const int64_t *mode_sizes, 
     for (long long l2 : {256LL, 384LL, 512LL, 768LL, 1024LL, 1536LL, 2048LL, 3072LL, 4096LL,
                          6144LL, 8192LL})
       for (long long l1 : {8LL, 12LL, 16LL, 24LL, 32LL, 48LL, 64LL, 96LL, 128LL, 192LL, 256LL,
-                           384LL, 512LL, 768LL, 1024LL, 1536LL, 2048LL}) {
+                           384LL, 512LL, 768LL, 1024LL, 1536LL, 2048LL, 3072LL, 4096LL}) {
         const long long l = l1 * l2;
         if (fft_len > 0 ? l != fft_len : l < d) continue;
         // smallest L; on ties prefer rows with a fast kernel, then fewer columns
@@ -497,7 +499,7 @@ int hk_plan_create_block(hk_plan **plan, int order, int levels, const int64_t *l
     L1 = fft_lens[1];
   } else {
     for (long long l1 : {8LL, 12LL, 16LL, 24LL, 32LL, 48LL, 64LL, 96LL, 128LL, 192LL, 256LL,
-                         384LL, 512LL, 768LL, 1024LL, 1536LL, 2048LL})
+                         384LL, 512LL, 768LL, 1024LL, 1536LL, 2048LL, 3072LL, 4096LL})
       if (l1 >= dout) {
         L1 = l1;
         break;

@@ -350,6 +350,9 @@ static cudaError_t launch_cols_stage(const ColArgs &a, long long items, int ncol
     HK_COL(1024, 2, Plan1D<1024, 64, 4, 16, 16>)
     HK_COL(1536, 4, Plan1D<1536, 96, 6, 16, 16>)
     HK_COL(2048, 2, Plan1D<2048, 128, 8, 16, 16>)
+    // d_H beyond 2048 x 8192 = 2^24: one-column tiles of 3072 / 4096 rows
+    HK_COL(3072, 1, Plan1D<3072, 192, 12, 16, 16>)
+    HK_COL(4096, 1, Plan1D<4096, 256, 16, 16, 16>)
 #undef HK_COL
     default:
       return cudaErrorNotSupported;
@@ -362,6 +365,7 @@ bool supported_col_len(long long L1) {
   switch (L1) {
     case 8: case 12: case 16: case 24: case 32: case 48: case 64: case 96: case 128:
     case 192: case 256: case 384: case 512: case 768: case 1024: case 1536: case 2048:
+    case 3072: case 4096:
       return true;
     default:
       return false;

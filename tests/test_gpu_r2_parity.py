@@ -165,3 +165,22 @@ def test_multi_device_sharded_product_matches_golden():
         assert strict_relerr(y[s], g["y"][k]) <= 1e-10
     norms = np.linalg.norm(y, axis=1)
     assert np.max(np.abs(norms - g["norms"][:64]) / g["norms"][:64]) <= 1e-10
+
+
+@pytest.mark.parametrize("shape,real", [((10_000_000, 8_000_000), False),
+                                        ((6_000_000,) * 3, True)])
+def test_lengths_beyond_2_24(shape, real):
+    """d_H ~ 1.8e7 > 2^24: four-step with a 3072-row column plan (L = 3072 x 8192)."""
+    rng = np.random.default_rng(24)
+    d = sum(shape) - len(shape) + 1
+    mk = (lambda n: rng.standard_normal(n)) if real else (lambda n: rand_vec(rng, n))
+    h = mk(d)
+    xs = [mk(n) for n in shape[1:]]
+    dh = torch.from_numpy(h).cuda()[None]
+    dxs = [torch.from_numpy(x).cuda()[None] for x in xs]
+    if len(xs) == 2:
+        dxs = [dxs[0], dxs[0]]
+        xs = [xs[0], xs[0]]
+    y = batched.hankel_tvp_partial(dh, dxs, shape)[0].cpu().numpy()
+    ref = O.hankel_tvp_partial_padded(h, shape, xs)
+    assert strict_relerr(y, ref) <= 1e-10
