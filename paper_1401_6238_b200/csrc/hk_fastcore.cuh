@@ -115,6 +115,13 @@ template <class T>
 struct ChunkOf<T, std::void_t<decltype(T::kChunk)>> {
   static constexpr int value = T::kChunk;
 };
+// Twiddle sources that also hold the pass-1 twiddles (a per-thread TMEM slab)
+// expose chunk1(c, w): W_{Lp}^{j lo}, j = 4c+1 .. 4c+4, of this thread's pass-1
+// butterfly.
+template <class T, class = void>
+struct HasChunk1 : std::false_type {};
+template <class T>
+struct HasChunk1<T, std::void_t<decltype(&T::chunk1)>> : std::true_type {};
 
 // Pass-0 twiddles by recurrence: W_L^{j beta} = (W_L^beta)^j from one table
 // read per butterfly (two interleaved chains, <= 8 products deep), trading
@@ -176,7 +183,10 @@ __device__ __forceinline__ void pass(int t, const C *__restrict__ tw, const TW0 
   constexpr int NBUT = PL::L / R;
   constexpr int NB = (NBUT + PL::T - 1) / PL::T;
   constexpr int H = Tr::hi_count(p);
-  constexpr bool HIM = Tr::hi_major(p);
+  // hi-major order makes a warp's table reads of the pass-p twiddles broadcast;
+  // with per-thread twiddle slabs (HasChunk1) the lo-major order is used, which
+  // keeps the pass P-2 -> P-1 exchange inside each warp (see fft_dif).
+  constexpr bool HIM = Tr::hi_major(p) && !HasChunk1<TW0>::value;
   constexpr int NIN = FINAL ? R : NZ;
   constexpr int NOUT = FINAL ? NO : R;
   // Pass-0 recurrence bases of a thread's NB butterflies, beta = t + i*T:
@@ -232,6 +242,16 @@ __device__ __forceinline__ void pass(int t, const C *__restrict__ tw, const TW0 
             tw0.chunk(beta, c, w);
             sfor<CK>([&](auto qc) {
               constexpr int j = CK * c + decltype(qc)::value + 1;
+              if constexpr (j < R) a[j] = cmul_dir<INV>(a[j], w[decltype(qc)::value]);
+            });
+          });
+        } else if constexpr (p == 1 && PL::P == 3 && HasChunk1<TW0>::value) {
+          sfor<(R - 1 + 3) / 4>([&](auto cc) {
+            constexpr int c = decltype(cc)::value;
+            C w[4];
+            tw0.chunk1(c, w);
+            sfor<4>([&](auto qc) {
+              constexpr int j = 4 * c + decltype(qc)::value + 1;
               if constexpr (j < R) a[j] = cmul_dir<INV>(a[j], w[decltype(qc)::value]);
             });
           });
@@ -311,11 +331,23 @@ struct NoHook {
 
 // hook() runs (on every thread) right after the barrier that follows pass 0,
 // i.e. once every thread of the group has consumed the pass-0 input.
+//
+// WSync (if not void) replaces the group barrier before the last pass.  Valid
+// when that exchange stays inside each warp: lo-major pass P-2 with
+// radix[P-2] == radix[P-1] and 32 % radix[P-1] == 0 -- warp w then writes and
+// reads exactly positions [32 w R, 32 (w + 1) R) (R the last radix).
 template <class PL, bool INV, int NZ, int TWL = PL::L, bool REC = false, class TW0, class GLoad,
-          class Sync = CtaSync, class Hook = NoHook, class C>
+          class Sync = CtaSync, class Hook = NoHook, class WSync = void, class C>
 __device__ __forceinline__ void fft_dif(C *sbuf, int t, const C *__restrict__ tw,
                                         const TW0 &tw0, GLoad &&gload, C (&out)[PL::V],
-                                        Sync sync = Sync(), Hook hook = Hook()) {
+                                        Sync sync = Sync(), Hook hook = Hook(),
+                                        WSync * = nullptr) {
+  auto last_sync = [&]() {
+    if constexpr (std::is_void_v<WSync>)
+      sync();
+    else
+      WSync()();
+  };
   constexpr int RL = PL::Rlast;
   constexpr int R0 = PL::radix[0];
   // gload(pos), or gload(i, j, pos) for loaders that need the butterfly slot
@@ -344,17 +376,30 @@ __device__ __forceinline__ void fft_dif(C *sbuf, int t, const C *__restrict__ tw
     pass<PL, q, INV, false, PL::radix[q], PL::radix[q], TWL, REC, TW0, SL, SS>(t, tw, tw0, s_load,
                                                                           s_store);
   });
-  sync();
-  if constexpr (PL::P == 2) hook();
+  if constexpr (PL::P == 2) {
+    sync();
+    hook();
+  } else {
+    last_sync();
+  }
   pass<PL, PL::P - 1, INV, false, RL, RL, TWL, REC, TW0, SL, decltype(r_store) &>(t, tw, tw0, s_load,
                                                                              r_store);
 }
 
+// WSync (if not void): the entry barrier and the pass P-1 -> P-2 exchange stay
+// inside each warp (same condition as fft_dif; the entry barrier only orders
+// against the previous transform's last-pass reads, which were warp-local).
 template <class PL, int NO, int TWL = PL::L, bool REC = false, class TW0, class GStore,
-          class Sync = CtaSync, class C>
+          class Sync = CtaSync, class WSync = void, class C>
 __device__ __forceinline__ void fft_final(C *sbuf, int t, const C *__restrict__ tw,
                                           const TW0 &tw0, C (&in)[PL::V], GStore &&gstore,
-                                          Sync sync = Sync()) {
+                                          Sync sync = Sync(), WSync * = nullptr) {
+  auto warp_sync = [&]() {
+    if constexpr (std::is_void_v<WSync>)
+      sync();
+    else
+      WSync()();
+  };
   constexpr int RL = PL::Rlast;
   constexpr int R0 = PL::radix[0];
   auto r_load = [&](int i, int j, int) { return in[i * RL + j]; };
@@ -364,14 +409,17 @@ __device__ __forceinline__ void fft_final(C *sbuf, int t, const C *__restrict__ 
   const SmemIO sio{smem_u32(sbuf)};
   auto &&s_load = pick_io<PL, C>(s_load_l, sio);
   auto &&s_store = pick_io<PL, C>(s_store_l, sio);
-  sync();
+  warp_sync();
   using SL = decltype(s_load);
   using SS = decltype(s_store);
   pass<PL, PL::P - 1, false, true, RL, RL, TWL, REC, TW0, decltype(r_load) &, SS>(t, tw, tw0, r_load,
                                                                              s_store);
   sfor<PL::P - 2>([&](auto qc) {
     constexpr int q = PL::P - 2 - decltype(qc)::value;
-    sync();
+    if constexpr (q == PL::P - 2)
+      warp_sync();
+    else
+      sync();
     pass<PL, q, false, true, PL::radix[q], PL::radix[q], TWL, REC, TW0, SL, SS>(t, tw, tw0, s_load,
                                                                            s_store);
   });

@@ -81,6 +81,15 @@ struct Tw0Tmem8 {
   __device__ __forceinline__ void chunk(int, int c, cplx *w) const { tmem_ld8(taddr + 32 * c, w); }
 };
 
+// Both twiddle sets from TMEM: pass 0 (W_L^{j t}) and pass 1 (W_{L/R0}^{j lo}).
+// A thread's twiddles depend only on its index in its group, so the two
+// groups' warps that share a TMEM lane quadrant and an index share one slab.
+struct Tw01Tmem {
+  uint32_t taddr0, taddr1;
+  __device__ __forceinline__ void chunk(int, int c, cplx *w) const { tmem_ld4(taddr0 + 16 * c, w); }
+  __device__ __forceinline__ void chunk1(int c, cplx *w) const { tmem_ld4(taddr1 + 16 * c, w); }
+};
+
 template <class PL>
 struct Layout {
   static constexpr int L = PL::L;
@@ -90,7 +99,8 @@ struct Layout {
 };
 
 // TWV bit 0: pass-0 twiddles by recurrence from W_L^t (else the TMEM slab);
-// bit 1: pass->=1 twiddles by recurrence from one compact-table read.
+// bit 1: pass->=1 twiddles by recurrence from one compact-table read;
+// bit 3: pass-1 twiddles from TMEM too (slabs shared by the two groups).
 template <class PL, int NZ, int NO, int TWV>
 __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constant__ Args1D a) {
   constexpr bool REC = (TWV & 2) != 0;
@@ -129,10 +139,44 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
   tmem_fence_after();
   const uint32_t lane_q = (uint32_t)(32 * (warp & 3)) << 16;
   const uint32_t tacc = tmem_slot + lane_q + (uint32_t)((warp >> 2) * 64);
-  const uint32_t ttw = tmem_slot + lane_q + 256u + (uint32_t)((warp >> 2) * 64);
+  constexpr bool TW1T = (TWV & 8) != 0;
+  // with TW1T the pass-0 slab of the thread index t_in is shared by both groups
+  // (cols 256 + 64 * ((warp >> 2) & 1)) and the pass-1 slab sits at 384 + ...
+  const uint32_t ttw = tmem_slot + lane_q + 256u +
+                       (uint32_t)((TW1T ? ((warp >> 2) & 1) : (warp >> 2)) * 64);
+  const uint32_t ttw1 = ttw + 128u;
 
-  // this thread's first-pass twiddles W_L^{j t} -> TMEM (same for every product)
-  if constexpr (!(TWV & 1)) {
+  if constexpr (TW1T) {
+    static_assert(!(TWV & 1) && PL::P == 3, "pass-1 TMEM twiddles need the pass-0 slab too");
+    if (g == 0) {
+      const fast::Tw0Global g0{a.tw0, L / R0, R0};
+      // pass-1 butterfly of thread t (lo-major with TMEM twiddles, see
+      // fast::pass): lo = t mod stride(1), twiddles W_{L/R0}^{j lo}
+      constexpr int R1 = PL::radix[1];
+      const int lo1 = t_in % PL::stride(1);
+#pragma unroll
+      for (int c = 0; c < (R0 - 1 + 3) / 4; ++c) {
+        cplx w[4];
+        g0.chunk(t_in, c, w);
+        tmem_st4(ttw + 16 * c, w);
+      }
+#pragma unroll
+      for (int c = 0; c < (R1 - 1 + 3) / 4; ++c) {
+        cplx w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = 4 * c + q + 1;
+          w[q] = j < R1 ? a.tw1[(j * lo1) % TW1] : make_double2(1.0, 0.0);
+        }
+        tmem_st4(ttw1 + 16 * c, w);
+      }
+      tmem_wait_st();
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+  } else if constexpr (!(TWV & 1)) {
+    // this thread's first-pass twiddles W_L^{j t} -> TMEM (same for every product)
     const fast::Tw0Global g0{a.tw0, L / R0, R0};
 #pragma unroll
     for (int c = 0; c < (R0 - 1 + 3) / 4; ++c) {
@@ -142,10 +186,14 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
     }
     tmem_wait_st();
   }
-  using TW0 = std::conditional_t<(TWV & 1) != 0, fast::Tw0Rec,
-                                 std::conditional_t<(TWV & 4) != 0, Tw0Tmem8, Tw0Tmem>>;
+  using TW0 = std::conditional_t<
+      TW1T, Tw01Tmem,
+      std::conditional_t<(TWV & 1) != 0, fast::Tw0Rec,
+                         std::conditional_t<(TWV & 4) != 0, Tw0Tmem8, Tw0Tmem>>>;
   TW0 tw0;
-  if constexpr ((TWV & 1) != 0)
+  if constexpr (TW1T)
+    tw0 = Tw01Tmem{ttw, ttw1};
+  else if constexpr ((TWV & 1) != 0)
     tw0 = fast::Tw0Rec{a.tw};
   else
     tw0 = TW0{ttw};
@@ -175,6 +223,11 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
     }
   }
 
+  // lo-major pass 1 keeps the pass-1 <-> pass-2 exchanges inside each warp:
+  // those barriers become warp syncs (fast::fft_dif / fft_final)
+  using WS = std::conditional_t<TW1T, fast::WarpSync, void>;
+  static_assert(!TW1T || (PL::radix[1] == PL::Rlast && 32 % PL::Rlast == 0),
+                "warp-local exchange needs equal last two radices");
   auto run = [&](auto gc) {
     constexpr int G = decltype(gc)::value;
     const NamedSync<1 + G, T> sync;
@@ -208,7 +261,8 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
                            (blockIdx.x + (k + 1) * gridDim.x) * a.h.bstride,
                        bytes, mb);
             }
-          });
+          },
+          (WS *)nullptr);
       tmem_wait_st();
 #pragma unroll
       for (int c = 0; c < V / 4; ++c) tmem_st4(tacc + 16 * c, &v[4 * c]);
@@ -228,7 +282,8 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
                            (blockIdx.x + (k + 2) * gridDim.x) * a.fac[0].bstride,
                        bytes, mb);
             }
-          });
+          },
+          (WS *)nullptr);
       tmem_wait_st();
 #pragma unroll
       for (int c = 0; c < V / 4; ++c) {
@@ -250,7 +305,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
               static_cast<cplx *>(a.out)[(blockIdx.x + k * gridDim.x) * a.out_bstride + pos] =
                   make_double2(val.x * a.scale, val.y * a.scale);
           },
-          sync);
+          sync, (WS *)nullptr);
     }
   };
   if (g == 0)
@@ -308,10 +363,11 @@ cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream) {
   using PL = Plan1D<4096, 256, 16, 16, 16>;
   constexpr int s0 = PL::stride(0);
   const int nz = (x.len + s0 - 1) / s0, no = (a.out_len + s0 - 1) / s0;
-  int twv = 2;  // measured best on B200 (cfg2): TMEM pass 0, recurrence passes >= 1
-  if (const char *e = getenv("HK_PP_TWV")) twv = atoi(e) & 7;
+  int twv = 8;  // TMEM pass-0 and pass-1 twiddles (r02); 2 = recurrence for pass 1 (r01)
+  if (const char *e = getenv("HK_PP_TWV")) twv = atoi(e) & 15;
   if (nz <= 4 && no <= 4) {
     switch (twv) {
+      case 8: return pp::launch_pp<PL, 4, 4, 8>(a, stream);
       case 6: return pp::launch_pp<PL, 4, 4, 6>(a, stream);
       case 1: return pp::launch_pp<PL, 4, 4, 1>(a, stream);
       case 2: return pp::launch_pp<PL, 4, 4, 2>(a, stream);
