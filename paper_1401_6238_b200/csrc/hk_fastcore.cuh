@@ -115,6 +115,10 @@ template <class T>
 struct ChunkOf<T, std::void_t<decltype(T::kChunk)>> {
   static constexpr int value = T::kChunk;
 };
+struct NoHookT {
+  __device__ __forceinline__ void operator()() const {}
+};
+
 // Twiddle sources that also hold the pass-1 twiddles (a per-thread TMEM slab)
 // expose chunk1(c, w): W_{Lp}^{j lo}, j = 4c+1 .. 4c+4, of this thread's pass-1
 // butterfly.
@@ -173,9 +177,9 @@ struct Tw0Global {
 // shared-memory carve-out (the strided reads of a W_L table touch one 128-B
 // line per twiddle).
 template <class PL, int p, bool INV, bool FINAL, int NZ, int NO, int TWL = PL::L, bool REC = false,
-          class TW0, class Load, class Store, class C>
+          class TW0, class Load, class Store, class C, class PreStore = NoHookT>
 __device__ __forceinline__ void pass(int t, const C *__restrict__ tw, const TW0 &tw0,
-                                     Load &&load, Store &&store) {
+                                     Load &&load, Store &&store, PreStore pre_store = PreStore()) {
   using Tr = Traits<PL>;
   constexpr int R = PL::radix[p];
   constexpr int s = PL::stride(p);
@@ -282,6 +286,7 @@ __device__ __forceinline__ void pass(int t, const C *__restrict__ tw, const TW0 
         DftP<R, INV, NZ, R>::run(a);
         twiddle();
       }
+      pre_store();
       if constexpr (std::is_same_v<std::decay_t<Store>, SmemIO>) {
         const HexAddr<Q> ad(store.sbase, base);
         sfor<NOUT>([&](auto jc) {
@@ -328,6 +333,11 @@ using GroupSync = std::conditional_t<(PL::T <= 32 && 32 % PL::T == 0), WarpSync,
 struct NoHook {
   __device__ __forceinline__ void operator()() const {}
 };
+// Default entry of fft_dif: a group barrier before pass 0 (orders its stores
+// after the previous transform's reads of the exchange buffer).  Any other
+// Entry object is called instead right before the pass-0 stores (a split
+// arrive/wait barrier whose wait then overlaps the pass-0 loads and math).
+struct SyncEntry {};
 
 // hook() runs (on every thread) right after the barrier that follows pass 0,
 // i.e. once every thread of the group has consumed the pass-0 input.
@@ -337,11 +347,13 @@ struct NoHook {
 // radix[P-2] == radix[P-1] and 32 % radix[P-1] == 0 -- warp w then writes and
 // reads exactly positions [32 w R, 32 (w + 1) R) (R the last radix).
 template <class PL, bool INV, int NZ, int TWL = PL::L, bool REC = false, class TW0, class GLoad,
-          class Sync = CtaSync, class Hook = NoHook, class WSync = void, class C>
+          class Sync = CtaSync, class Hook = NoHook, class WSync = void, class Entry = SyncEntry,
+          class C>
 __device__ __forceinline__ void fft_dif(C *sbuf, int t, const C *__restrict__ tw,
                                         const TW0 &tw0, GLoad &&gload, C (&out)[PL::V],
                                         Sync sync = Sync(), Hook hook = Hook(),
-                                        WSync * = nullptr) {
+                                        WSync * = nullptr, Entry entry = Entry()) {
+  constexpr bool kEntrySync = std::is_same_v<Entry, SyncEntry>;
   auto last_sync = [&]() {
     if constexpr (std::is_void_v<WSync>)
       sync();
@@ -364,11 +376,15 @@ __device__ __forceinline__ void fft_dif(C *sbuf, int t, const C *__restrict__ tw
   auto &&s_load = pick_io<PL, C>(s_load_l, sio);
   auto &&s_store = pick_io<PL, C>(s_store_l, sio);
   static_assert(PL::P >= 2, "fast path needs at least two passes");
-  sync();
+  if constexpr (kEntrySync) sync();
   using SL = decltype(s_load);
   using SS = decltype(s_store);
-  pass<PL, 0, INV, false, (NZ < R0 ? NZ : R0), R0, TWL, REC, TW0, decltype(g_load) &, SS>(
-      t, tw, tw0, g_load, s_store);
+  if constexpr (kEntrySync)
+    pass<PL, 0, INV, false, (NZ < R0 ? NZ : R0), R0, TWL, REC, TW0, decltype(g_load) &, SS>(
+        t, tw, tw0, g_load, s_store);
+  else
+    pass<PL, 0, INV, false, (NZ < R0 ? NZ : R0), R0, TWL, REC, TW0, decltype(g_load) &, SS, C,
+         Entry &>(t, tw, tw0, g_load, s_store, entry);
   sfor<PL::P - 2>([&](auto qc) {
     constexpr int q = decltype(qc)::value + 1;
     sync();

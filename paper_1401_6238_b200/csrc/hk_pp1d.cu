@@ -62,6 +62,24 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint32_t addr) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(addr) : "memory");
+}
+// Split WAR barrier of a product group: every warp arrives (one lane, after
+// the loaded values were consumed) once it has finished reading the exchange
+// buffer; the next writer waits only right before its first stores.
+struct WarWait {
+  uint32_t addr, parity;
+  bool on;
+  __device__ __forceinline__ void operator()() const {
+    if (on) mbar_wait(addr, parity);
+  }
+};
+__device__ __forceinline__ void war_arrive(uint32_t addr) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(addr);
+}
+
 template <int ID, int N>
 struct NamedSync {
   __device__ __forceinline__ void operator()() const {
@@ -110,7 +128,10 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
   constexpr int TW1 = L / R0;  // passes >= 1 read the compact W_{L/R0} table
   (void)Layout<PL>{};
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t mbar[4];  // full_h[0..1], full_x[0..1]
+  // full_h[0..1], full_x[0..1] (TMA arrivals); war_x[0..1], war_h[0..1] (split
+  // WAR barriers of group G: h pass-2 reads -> x pass-0 stores, final pass-0
+  // reads -> next h pass-0 stores; used with TW1T)
+  __shared__ __align__(8) uint64_t mbar[8];
   __shared__ uint32_t tmem_slot;
   cplx *ex = reinterpret_cast<cplx *>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
   cplx *hst = ex + 2 * L;
@@ -120,6 +141,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
   const int g = threadIdx.x / T;
   const int t_in = threadIdx.x - g * T;
   const uint32_t mb_h0 = smem_u32(&mbar[0]), mb_x0 = smem_u32(&mbar[2]);
+  const uint32_t mb_wx0 = smem_u32(&mbar[4]), mb_wh0 = smem_u32(&mbar[6]);
 
   // The TMA only ever writes the first h.len (x.len) staged elements: zero the
   // tails once so the first passes read the zero padding without bounds tests.
@@ -132,6 +154,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
   if (warp == 0) tmem_alloc<512>(&tmem_slot);
   if (threadIdx.x == 32) {
     for (int i = 0; i < 4; ++i) mbar_init(smem_u32(&mbar[i]), 1);
+    for (int i = 4; i < 8; ++i) mbar_init(smem_u32(&mbar[i]), T / 32);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   tmem_fence_before();
@@ -228,8 +251,24 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
   using WS = std::conditional_t<TW1T, fast::WarpSync, void>;
   static_assert(!TW1T || (PL::radix[1] == PL::Rlast && 32 % PL::Rlast == 0),
                 "warp-local exchange needs equal last two radices");
+  // TWV bit 4: the two WAR barriers of a product (entries of the h and x
+  // transforms) become split mbarrier arrive/wait pairs
+  constexpr bool SPLIT = TW1T && (TWV & 16) != 0;
+  using Entry = std::conditional_t<SPLIT, WarWait, fast::SyncEntry>;
   auto run = [&](auto gc) {
     constexpr int G = decltype(gc)::value;
+    auto h_entry = [&](int kk) {
+      if constexpr (SPLIT)
+        return Entry{mb_wh0 + 8 * G, (uint32_t)((kk - 1) & 1), kk > 0};
+      else
+        return Entry{};
+    };
+    auto x_entry = [&](int kk) {
+      if constexpr (SPLIT)
+        return Entry{mb_wx0 + 8 * G, (uint32_t)(kk & 1), true};
+      else
+        return Entry{};
+    };
     const NamedSync<1 + G, T> sync;
     cplx *sbuf = ex + G * L;
     cplx *my_x = xst + G * XS;
@@ -262,7 +301,8 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
                        bytes, mb);
             }
           },
-          (WS *)nullptr);
+          (WS *)nullptr, h_entry(kk));
+      if constexpr (SPLIT) war_arrive(mb_wx0 + 8 * G);
       tmem_wait_st();
 #pragma unroll
       for (int c = 0; c < V / 4; ++c) tmem_st4(tacc + 16 * c, &v[4 * c]);
@@ -283,7 +323,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
                        bytes, mb);
             }
           },
-          (WS *)nullptr);
+          (WS *)nullptr, x_entry(kk));
       tmem_wait_st();
 #pragma unroll
       for (int c = 0; c < V / 4; ++c) {
@@ -306,6 +346,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
                   make_double2(val.x * a.scale, val.y * a.scale);
           },
           sync, (WS *)nullptr);
+      if constexpr (SPLIT) war_arrive(mb_wh0 + 8 * G);
     }
   };
   if (g == 0)
@@ -363,11 +404,14 @@ cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream) {
   using PL = Plan1D<4096, 256, 16, 16, 16>;
   constexpr int s0 = PL::stride(0);
   const int nz = (x.len + s0 - 1) / s0, no = (a.out_len + s0 - 1) / s0;
-  int twv = 8;  // TMEM pass-0 and pass-1 twiddles (r02); 2 = recurrence for pass 1 (r01)
-  if (const char *e = getenv("HK_PP_TWV")) twv = atoi(e) & 15;
+  // 24: TMEM pass-0 and pass-1 twiddles + split WAR barriers (r02: 169.4 us vs
+  // 170.0 for 8 and 185.6 for 2 = recurrence for pass 1, the r01 default)
+  int twv = 24;
+  if (const char *e = getenv("HK_PP_TWV")) twv = atoi(e) & 31;
   if (nz <= 4 && no <= 4) {
     switch (twv) {
       case 8: return pp::launch_pp<PL, 4, 4, 8>(a, stream);
+      case 24: return pp::launch_pp<PL, 4, 4, 24>(a, stream);
       case 6: return pp::launch_pp<PL, 4, 4, 6>(a, stream);
       case 1: return pp::launch_pp<PL, 4, 4, 1>(a, stream);
       case 2: return pp::launch_pp<PL, 4, 4, 2>(a, stream);
