@@ -1,0 +1,395 @@
+// K3t: TMA-fed column passes of the 1D four-step for the real-operand product
+// (cfg3, reference hankel.py:140-147 at L = 1536 x 8192).
+//
+// The generic column kernel (hk_large.cu) streams its tiles with per-thread
+// 8/16-byte cp.async and stores them with per-element index arithmetic; on
+// cfg3 that integer work and its latency were 44% of the stall samples (ncu
+// source page, r02).  Here the Tensor Memory Accelerator moves each column
+// tile: ONE thread issues 2-D boxes [TILE columns x 256 rows] of the row-major
+// L1 x L2 view (zero fill past the operand), an mbarrier collects the bytes,
+// and the next tile's boxes land in a separate landing buffer while the
+// current tile is transformed in the exchange buffer.
+//
+//   ST_A_PAIR: z = h + i x (real h, real x), forward column DFT, split by
+//              conjugate symmetry into the stage-A outputs of h (inverse, 1/L,
+//              four-step twiddle) and x (forward, twiddle); rows k <= L1/2
+//              only when `half` (the Hermitian product, see hk_capi.cu).
+//   ST_C:      the final column pass over the row-stage output Q, rows above
+//              L1/2 synthesised from row L1 - k1 (Hermitian), truncated to y.
+//
+// Pass 0 reads the landing boxes with an interleaved thread mapping (lanes
+// run along the TILE columns of a row first: conflict-free 8/16-byte reads of
+// the packed boxes); passes >= 1 and the epilogue use the column-major mapping
+// of k_cols on the swizzled exchange buffer.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <atomic>
+#include <mutex>
+
+#include "hk_fastcore.cuh"
+#include "hk_large.h"
+
+namespace hk {
+namespace large {
+
+struct alignas(64) ColTma {
+  CUtensorMap m_in;   // ST_A_PAIR: h (f64 [items][rows][L2]); ST_C: Q (f64 pairs)
+  CUtensorMap m_in2;  // ST_A_PAIR: x
+  ColArgs a;
+  long long rows_in, rows_in2;  // full rows the maps cover (TMA zero-fills below)
+  long long tail_in, tail_in2;  // valid elements of the partial row after them
+};
+
+namespace tma {
+
+__device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(addr), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t addr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(addr), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void load3d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                       uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+}  // namespace tma
+
+__device__ __forceinline__ cplx tw4(const ColArgs &a, long long e) {
+  e %= a.L;
+  return cmul(__ldg(&a.thi[e >> 12]), __ldg(&a.tlo[e & 4095]));
+}
+
+template <class PL, int TILE, int STAGE>
+struct TmaLayout {
+  static constexpr int L1 = PL::L;
+  static constexpr int BR = 256;  // box rows
+  static constexpr int PAD = TILE >= 8 ? 1 : 8 / TILE;
+  static constexpr int CS = L1 + PAD;
+  static constexpr bool PAIR = STAGE == ST_A_PAIR;
+  // ST_C lands at most L1 complex rows (all of them without `half`)
+  static constexpr int LAND = PAIR ? 2 * L1 * TILE * 8 : L1 * TILE * 16;
+  static constexpr int EX = TILE * CS * 16;
+  static constexpr int SMEM = LAND + EX + 128;
+  static_assert(L1 % BR == 0, "column length must be a multiple of the box height");
+};
+
+template <class PL, int TILE, int STAGE>
+__global__ void __launch_bounds__(TILE * PL::T, 1)
+    k_cols_tma(const __grid_constant__ ColTma g, int tiles_per_item, long long ntiles) {
+  using LY = TmaLayout<PL, TILE, STAGE>;
+  constexpr int L1 = PL::L, T = PL::T, V = PL::V, RL = PL::Rlast, R0 = PL::radix[0];
+  constexpr int CS = LY::CS, BR = LY::BR, NT = TILE * T;
+  constexpr bool PAIR = LY::PAIR;
+  const ColArgs &a = g.a;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t mbar;
+  unsigned char *base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  double *land = reinterpret_cast<double *>(base);
+  cplx *landc = reinterpret_cast<cplx *>(base);
+  cplx *ex = reinterpret_cast<cplx *>(base + LY::LAND);
+  const uint32_t mb = smem_u32(&mbar);
+  const int lrows = PAIR ? L1 : (a.half ? ((L1 / 2 + 1 + BR - 1) / BR) * BR : L1);
+
+  auto issue = [&](long long w) {
+    const long long item = w / tiles_per_item;
+    const int c0 = (int)(w - item * tiles_per_item) * TILE;
+    if constexpr (PAIR) {
+      tma::mbar_expect_tx(mb, 2u * L1 * TILE * 8u);
+      for (int b = 0; b < L1 / BR; ++b) {
+        tma::load3d(smem_u32(land + b * BR * TILE), &g.m_in, c0, b * BR, (int)item, mb);
+        tma::load3d(smem_u32(land + (L1 + b * BR) * TILE), &g.m_in2, c0, b * BR, (int)item, mb);
+      }
+    } else {
+      tma::mbar_expect_tx(mb, (uint32_t)lrows * TILE * 16u);
+      for (int b = 0; b < lrows / BR; ++b)
+        tma::load3d(smem_u32(landc + b * BR * TILE), &g.m_in, 2 * c0, b * BR, (int)item, mb);
+    }
+  };
+
+  if (threadIdx.x == 0) {
+    tma::mbar_init(mb, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  long long w = blockIdx.x;
+  if (threadIdx.x == 0 && w < ntiles) issue(w);
+  const fast::Tw0Rec tw0{a.ctw};
+
+  for (int it = 0; w < ntiles; ++it, w += gridDim.x) {
+    const long long item = w / tiles_per_item;
+    const int c0 = (int)(w - item * tiles_per_item) * TILE;
+    tma::mbar_wait(mb, (uint32_t)(it & 1));
+    if constexpr (PAIR) {
+      // partial last rows of h and x (the maps cover full rows only)
+      if (threadIdx.x < 2 * TILE) {
+        const int c = threadIdx.x % TILE;
+        const bool second = threadIdx.x >= TILE;
+        const long long rows = second ? g.rows_in2 : g.rows_in;
+        const long long tail = second ? g.tail_in2 : g.tail_in;
+        if (tail > 0 && rows < L1) {
+          const Op2 &op = second ? a.in2 : a.in;
+          const int n2 = c0 + c;
+          const double v = n2 < tail ? static_cast<const double *>(op.ptr)[item * op.item_stride +
+                                                                           rows * a.L2 + n2]
+                                     : 0.0;
+          land[((second ? L1 : 0) + rows) * TILE + c] = v;
+        }
+      }
+      __syncthreads();
+    }
+    // ---- pass 0 from the landing boxes (interleaved mapping)
+    {
+      const int c = threadIdx.x % TILE, tp = threadIdx.x / TILE;
+      const int n2 = c0 + c;
+      cplx *col = ex + c * CS;
+      constexpr int S0 = PL::stride(0);
+      cplx tw_cur = make_double2(1.0, 0.0), tw_step = make_double2(1.0, 0.0), wrow = tw_step;
+      if constexpr (!PAIR) {
+        tw_step = tw4(a, (long long)n2 * S0);
+        if (a.half) wrow = tw4(a, (long long)n2 * L1);  // W_L2^{n2}
+      }
+      auto in_load = [&](int, int j, int pos) {
+        if constexpr (PAIR) {
+          return make_double2(land[pos * TILE + c], land[(L1 + pos) * TILE + c]);
+        } else {
+          cplx v;
+          if (a.half && 2 * pos > L1) {
+            // Q(L1-k1, m2) = conj(W_L2^{m2} Q(k1, m2))
+            v = cmul(landc[(L1 - pos) * TILE + c], wrow);
+            v.y = -v.y;
+          } else {
+            v = landc[pos * TILE + c];
+          }
+          v.x *= a.in.scale;
+          v.y *= a.in.scale;
+          if (j == 0) tw_cur = tw4(a, (long long)n2 * pos);
+          v = cmul(v, tw_cur);
+          tw_cur = cmul(tw_cur, tw_step);
+          return v;
+        }
+      };
+      auto s_store = [&](int, int, int pos, cplx v) { col[fast::swz2(pos)] = v; };
+      fast::pass<PL, 0, false, false, R0, R0>(tp, a.ctw, tw0, in_load, s_store);
+    }
+    __syncthreads();
+    // the landing buffer is consumed: stream the next tile in behind the math
+    if (threadIdx.x == 0 && w + gridDim.x < ntiles) {
+      tma::fence_proxy_async();
+      issue(w + gridDim.x);
+    }
+    const int c = threadIdx.x / T, t = threadIdx.x - (threadIdx.x / T) * T;
+    const int n2 = c0 + c;
+    cplx *col = ex + c * CS;
+    auto s_load = [&](int, int, int pos) { return col[fast::swz2(pos)]; };
+    auto s_store = [&](int, int, int pos, cplx v) { col[fast::swz2(pos)] = v; };
+    cplx v[V];
+    auto r_store = [&](int i, int j, int, cplx x) { v[i * RL + j] = x; };
+    sfor<PL::P - 2>([&](auto qc) {
+      constexpr int q = decltype(qc)::value + 1;
+      fast::pass<PL, q, false, false, PL::radix[q], PL::radix[q], L1, true>(t, a.ctw, tw0, s_load,
+                                                                           s_store);
+      __syncthreads();
+    });
+    fast::pass<PL, PL::P - 1, false, false, RL, RL, L1, true>(t, a.ctw, tw0, s_load, r_store);
+    __syncthreads();
+    // digit-reversed registers -> natural order: register j of butterfly beta
+    // holds frequency k = k(beta) + j * L1 / RL
+#pragma unroll
+    for (int i = 0; i < V / RL; ++i) {
+      const int beta = t + i * T;
+      int k0 = 0, mul = 1;
+      sfor<PL::P>([&](auto pc) {
+        constexpr int p = decltype(pc)::value;
+        constexpr int Rp = PL::radix[p], Sp = PL::stride(p);
+        k0 += (((beta * RL) / Sp) % Rp) * mul;
+        mul *= Rp;
+      });
+#pragma unroll
+      for (int j = 0; j < RL; ++j) col[k0 + j * (L1 / RL)] = v[i * RL + j];
+    }
+    __syncthreads();
+    if constexpr (PAIR) {
+      // Z(k) = H(k) + i X(k):  H(k) = (Z(k) + conj Z(-k)) / 2,
+      // X(k) = (Z(k) - conj Z(-k)) / 2i; h takes the inverse (conj H, 1/L)
+      // and both the four-step twiddle W_L^{+-n2 k}.  Twiddles by recurrence:
+      // W^{n2 (t + pT)} = W^{n2 t} (W^{n2 T})^p, W^{n2 (L1 - k)} = W_L2^{n2} conj W^{n2 k}.
+      constexpr int NP = (L1 / 2 + 1 + T - 1) / T;
+      cplx xa[NP], xb[NP];
+      const double sh = a.in.scale;
+      cplx wk = tw4(a, (long long)n2 * t);
+      const cplx wstep = tw4(a, (long long)n2 * T), wl1 = tw4(a, (long long)n2 * L1);
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        const int k = t + p * T;
+        if (k <= L1 / 2) {
+          const int kk = k == 0 ? 0 : L1 - k;
+          const cplx A = col[k], B = col[kk];
+          const cplx H = make_double2(0.5 * (A.x + B.x), 0.5 * (A.y - B.y));
+          const cplx X = make_double2(0.5 * (A.y + B.y), 0.5 * (B.x - A.x));
+          const cplx wkk = k == 0 ? wk : cmulc(wl1, wk);
+          const cplx hk = cmul(H, wk), hkk = cmulc(H, wkk);
+          xa[p] = cmul(X, wk);
+          xb[p] = cmul(make_double2(X.x, -X.y), wkk);
+          col[k] = make_double2(hk.x * sh, -hk.y * sh);
+          if (kk != k) col[kk] = make_double2(hkk.x * sh, hkk.y * sh);
+        }
+        wk = cmul(wk, wstep);
+      }
+      __syncthreads();
+      const int rows_out = a.out.e1;  // L1/2 + 1 with `half`, else L1
+      auto store_rows = [&](const Out2 &o) {
+        cplx *dst = static_cast<cplx *>(o.ptr) + item * o.item_stride + c0;
+        for (int idx = threadIdx.x; idx < TILE * rows_out; idx += NT) {
+          const int cc = idx % TILE, r = idx / TILE;
+          if (c0 + cc < a.L2) dst[r * o.s1 + cc] = ex[cc * CS + r];
+        }
+      };
+      store_rows(a.out);
+      __syncthreads();
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        const int k = t + p * T;
+        if (k > L1 / 2) continue;
+        col[k] = xa[p];
+        if (k != 0 && 2 * k != L1) col[L1 - k] = xb[p];
+      }
+      __syncthreads();
+      store_rows(a.out2);
+    } else {
+      // y(m2 + L2 k) for the rows k with m2 + L2 k < len
+      const Out2 &o = a.out;
+      const long long krows = (o.len - c0 + a.L2 - 1) / a.L2;
+      const int rows = (int)(krows < L1 ? krows : L1);
+      cplx *dst = static_cast<cplx *>(o.ptr) + item * o.item_stride + c0 * o.s2;
+      for (int idx = threadIdx.x; idx < TILE * rows; idx += NT) {
+        const int cc = idx % TILE, r = idx / TILE;
+        if ((long long)(c0 + cc) + (long long)a.L2 * r < o.len) dst[r * o.s1 + cc * o.s2] = ex[cc * CS + r];
+      }
+    }
+    __syncthreads();  // exchange buffer reused by the next tile's pass 0
+  }
+}
+
+using EncodeFn = PFN_cuTensorMapEncodeTiled_v12000;
+
+static EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// f64 view [items][rows][inner] with row stride `rs` and item stride `is`
+// (elements); box [bx, 256, 1].
+static bool encode(CUtensorMap *m, const void *ptr, long long inner, long long rows,
+                   long long items, long long rs, long long is, int bx) {
+  EncodeFn fn = encode_fn();
+  if (!fn || rows <= 0 || inner <= 0) return false;
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (rs * 8) % 16 || (is * 8) % 16) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)(items > 0 ? items : 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)(rs * 8), (cuuint64_t)((is > 0 ? is : rs * rows) * 8)};
+  cuuint32_t box[3] = {(cuuint32_t)bx, 256u, 1u};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void *>(ptr), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <class PL, int TILE, int STAGE>
+static cudaError_t launch_t(const ColTma &g, long long items, int ncols, cudaStream_t stream) {
+  using LY = TmaLayout<PL, TILE, STAGE>;
+  static std::atomic<unsigned long long> configured{0};
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(configured.load() & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(k_cols_tma<PL, TILE, STAGE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, LY::SMEM);
+    if (e != cudaSuccess) return e;
+    cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+    configured.fetch_or(bit);
+  }
+  const int tiles = (ncols + TILE - 1) / TILE;
+  const long long ntiles = (long long)tiles * items;
+  if (ntiles <= 0) return cudaSuccess;
+  const long long grid = std::min<long long>(ntiles, sms[dev & 63]);
+  k_cols_tma<PL, TILE, STAGE><<<(unsigned)grid, TILE * PL::T, LY::SMEM, stream>>>(g, tiles, ntiles);
+  return cudaGetLastError();
+}
+
+}  // namespace large
+
+// cudaErrorNotSupported unless the request is a 1D four-step column pass this
+// kernel implements (L1 = 1536, contiguous rows of length L2, f64 operands for
+// the packed pass, complex Q for the final pass).
+cudaError_t launch_cols_tma(int stage, const large::ColArgs &a, long long items, int ncols,
+                            cudaStream_t stream) {
+  using namespace large;
+  if (getenv("HK_NO_COLTMA")) return cudaErrorNotSupported;
+  if (!a.twiddle || a.L1 != 1536 || items > 65535) return cudaErrorNotSupported;
+  constexpr int TILE = 4;
+  using PL = Plan1D<1536, 96, 6, 16, 16>;
+  ColTma g{};
+  g.a = a;
+  const long long L2 = a.L2;
+  if (stage == ST_A_PAIR) {
+    const Op2 &h = a.in, &x = a.in2;
+    if (h.kind != FK_F64 || x.kind != FK_F64 || h.s1 != L2 || h.s2 != 1 || x.s1 != L2 ||
+        x.s2 != 1 || h.len < 0 || x.len < 0 || a.out.s2 != 1 || a.out2.s2 != 1)
+      return cudaErrorNotSupported;
+    g.rows_in = std::min<long long>(a.L1, h.len / L2);
+    g.tail_in = h.len - g.rows_in * L2;
+    g.rows_in2 = std::min<long long>(a.L1, x.len / L2);
+    g.tail_in2 = x.len - g.rows_in2 * L2;
+    if (g.tail_in >= L2 || g.tail_in2 >= L2) return cudaErrorNotSupported;
+    if (!encode(&g.m_in, h.ptr, L2, std::max<long long>(g.rows_in, 1), items, L2, h.item_stride,
+                TILE) ||
+        !encode(&g.m_in2, x.ptr, L2, std::max<long long>(g.rows_in2, 1), items, L2,
+                x.item_stride, TILE))
+      return cudaErrorNotSupported;
+    if (g.rows_in == 0 || g.rows_in2 == 0) return cudaErrorNotSupported;
+    return launch_t<PL, TILE, ST_A_PAIR>(g, items, ncols, stream);
+  }
+  if (stage == ST_C) {
+    const Op2 &q = a.in;
+    if (q.kind != FK_C128 || q.s1 != L2 || q.s2 != 1 || q.len >= 0 || q.e2 < ncols)
+      return cudaErrorNotSupported;
+    const long long rows = a.half ? a.L1 / 2 + 1 : a.L1;
+    if (q.e1 < rows || !encode(&g.m_in, q.ptr, 2 * L2, rows, items, 2 * L2, 2 * q.item_stride,
+                               2 * TILE))
+      return cudaErrorNotSupported;
+    return launch_t<PL, TILE, ST_C>(g, items, ncols, stream);
+  }
+  return cudaErrorNotSupported;
+}
+
+}  // namespace hk

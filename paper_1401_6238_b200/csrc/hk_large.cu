@@ -348,7 +348,12 @@ static cudaError_t launch_cols_stage(const ColArgs &a, long long items, int ncol
     HK_COL(512, 4, Plan1D<512, 32, 2, 16, 16>)
     HK_COL(768, 4, Plan1D<768, 48, 3, 16, 16>)
     HK_COL(1024, 2, Plan1D<1024, 64, 4, 16, 16>)
-    HK_COL(1536, 4, Plan1D<1536, 96, 6, 16, 16>)
+    case 1536:  // HK_COL1536_TILE: A/B of the column-tile width for cfg3
+      if (getenv("HK_COL1536_TILE") && atoi(getenv("HK_COL1536_TILE")) == 2)
+        return launch_cols_t<Plan1D<1536, 96, 6, 16, 16>, 2, STAGE>(a, items, ncols, stream);
+      if (getenv("HK_COL1536_TILE") && atoi(getenv("HK_COL1536_TILE")) == 1)
+        return launch_cols_t<Plan1D<1536, 96, 6, 16, 16>, 1, STAGE>(a, items, ncols, stream);
+      return launch_cols_t<Plan1D<1536, 96, 6, 16, 16>, 4, STAGE>(a, items, ncols, stream);
     HK_COL(2048, 2, Plan1D<2048, 128, 8, 16, 16>)
     // d_H beyond 2048 x 8192 = 2^24: one-column tiles of 3072 / 4096 rows
     HK_COL(3072, 1, Plan1D<3072, 192, 12, 16, 16>)
@@ -374,6 +379,10 @@ bool supported_col_len(long long L1) {
 
 cudaError_t launch_cols(int stage, const large::ColArgs &a, long long items, int ncols,
                         cudaStream_t stream) {
+  if (stage == large::ST_A_PAIR || stage == large::ST_C) {
+    const cudaError_t e = launch_cols_tma(stage, a, items, ncols, stream);
+    if (e != cudaErrorNotSupported) return e;
+  }
   switch (stage) {
     case large::ST_A_PAIR: return large::launch_cols_stage<large::ST_A_PAIR>(a, items, ncols, stream);
     case large::ST_A_FWD: return large::launch_cols_stage<large::ST_A_FWD>(a, items, ncols, stream);

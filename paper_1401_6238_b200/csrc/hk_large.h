@@ -58,6 +58,9 @@ struct ColArgs {
 bool supported_col_len(long long L1);
 cudaError_t launch_cols(int stage, const large::ColArgs &a, long long items, int ncols,
                         cudaStream_t stream);
+// TMA-fed column passes (hk_cols_tma.cu); cudaErrorNotSupported outside their shapes
+cudaError_t launch_cols_tma(int stage, const large::ColArgs &a, long long items, int ncols,
+                            cudaStream_t stream);
 cudaError_t launch_rowsum(const double2 *part, long long rows, double2 *out, long long n,
                           cudaStream_t stream);
 
