@@ -40,6 +40,7 @@ struct hk_plan {
   const double2 *thi = nullptr, *tlo = nullptr;    // four-step twiddles
   const double2 *ctw = nullptr, *ctw0 = nullptr;   // column plan tables (L1)
   const double2 *rtw = nullptr, *rtw0 = nullptr;   // row plan tables (L2)
+  const double2 *rtw1 = nullptr;                     // row plan compact W_{L2/R0} table
   // block plans: inner (block) and outer sizes per mode
   std::vector<int64_t> inner, outer;
 };
@@ -429,7 +430,12 @@ int hk_plan_create_hankel(hk_plan **plan, int order, const int64_t *mode_sizes, 
         // HK_ROW_LEN: A/B knob preferring a row length among equal-L splits
         // (B200 cfg3: 1536 x 8192 877 us, 2048 x 6144 1087 us)
         static const long long want2 = getenv("HK_ROW_LEN") ? atoll(getenv("HK_ROW_LEN")) : 0;
-        const bool pref = want2 > 0 && l2 == want2, bpref = want2 > 0 && best2 == want2;
+        // default: 4096-point rows (two resident row CTAs per SM: B200 cfg3 row
+        // stage 137 vs 205 us for 8192) when the TMA column kernel covers L1
+        auto prefer = [&](long long c1, long long c2) {
+          return want2 > 0 ? c2 == want2 : (c2 == 4096 && hk::tma_col_len(c1));
+        };
+        const bool pref = prefer(l1, l2), bpref = best1 && prefer(best1, best2);
         if (!best1 || l < best1 * best2 ||
             (l == best1 * best2 &&
              (pref > bpref ||
@@ -450,7 +456,7 @@ int hk_plan_create_hankel(hk_plan **plan, int order, const int64_t *mode_sizes, 
     p->L2 = best2;
     p->L = {best1 * best2};
     const long long Lt = best1 * best2;
-    rc = line_tables(dev, best2, &p->rtw, &p->rtw0);
+    rc = line_tables(dev, best2, &p->rtw, &p->rtw0, &p->rtw1);
     if (!rc) rc = col_tables(dev, best1, &p->ctw, &p->ctw0);
     if (!rc) rc = get_twiddles_step(dev, Lt, 4096, (Lt + 4095) / 4096, &p->thi);
     if (!rc) rc = get_twiddles_step(dev, Lt, 1, 4096, &p->tlo);
@@ -575,7 +581,9 @@ namespace {
 
 int launch_row(long long L2, const Args1D &a, cudaStream_t st) {
   cudaError_t e = cudaErrorNotSupported;
-  if (!g_force_generic) e = hk::launch_fast_1d((int)L2, a, st);
+  // 4096-point rows: the TMA ping-pong kernel (two row products per SM)
+  if (!g_force_generic && a.tw1) e = hk::launch_pp_1d((int)L2, a, st);
+  if (!g_force_generic && e == cudaErrorNotSupported) e = hk::launch_fast_1d((int)L2, a, st);
   if (e == cudaErrorNotSupported) e = hk::launch_1d((int)L2, a, st);
   if (e != cudaSuccess) return cuda_fail(e, "row-stage kernel launch");
   return HK_OK;
@@ -742,6 +750,7 @@ int tl_run(const hk_plan *p, const hk_operand &h, const hk_operand *xs, int nx, 
     a.nsub = rows_b;
     a.tw = p->rtw;
     a.tw0 = p->rtw0;
+    a.tw1 = p->rtw1;
     a.scale = 1.0;
     a.prefetch = 1;
     a.h.ptr = whp;

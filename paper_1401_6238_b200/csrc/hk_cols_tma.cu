@@ -101,7 +101,11 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
   constexpr int L1 = PL::L, T = PL::T, V = PL::V, RL = PL::Rlast, R0 = PL::radix[0];
   constexpr int CS = LY::CS, BR = LY::BR, NT = TILE * T;
   constexpr bool PAIR = LY::PAIR;
+  constexpr bool SC = STAGE == ST_C;
+  constexpr bool INV = STAGE == ST_A_INV;
   const ColArgs &a = g.a;
+  // single-operand stage A: complex (16-byte) or real (8-byte) landing rows
+  const bool cin = SC || (!PAIR && a.in.kind == FK_C128);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t mbar;
   unsigned char *base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
@@ -109,7 +113,7 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
   cplx *landc = reinterpret_cast<cplx *>(base);
   cplx *ex = reinterpret_cast<cplx *>(base + LY::LAND);
   const uint32_t mb = smem_u32(&mbar);
-  const int lrows = PAIR ? L1 : (a.half ? ((L1 / 2 + 1 + BR - 1) / BR) * BR : L1);
+  const int lrows = (SC && a.half) ? ((L1 / 2 + 1 + BR - 1) / BR) * BR : L1;
 
   auto issue = [&](long long w) {
     const long long item = w / tiles_per_item;
@@ -120,10 +124,14 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
         tma::load3d(smem_u32(land + b * BR * TILE), &g.m_in, c0, b * BR, (int)item, mb);
         tma::load3d(smem_u32(land + (L1 + b * BR) * TILE), &g.m_in2, c0, b * BR, (int)item, mb);
       }
-    } else {
+    } else if (cin) {
       tma::mbar_expect_tx(mb, (uint32_t)lrows * TILE * 16u);
       for (int b = 0; b < lrows / BR; ++b)
         tma::load3d(smem_u32(landc + b * BR * TILE), &g.m_in, 2 * c0, b * BR, (int)item, mb);
+    } else {
+      tma::mbar_expect_tx(mb, (uint32_t)lrows * TILE * 8u);
+      for (int b = 0; b < lrows / BR; ++b)
+        tma::load3d(smem_u32(land + b * BR * TILE), &g.m_in, c0, b * BR, (int)item, mb);
     }
   };
 
@@ -140,20 +148,24 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
     const long long item = w / tiles_per_item;
     const int c0 = (int)(w - item * tiles_per_item) * TILE;
     tma::mbar_wait(mb, (uint32_t)(it & 1));
-    if constexpr (PAIR) {
-      // partial last rows of h and x (the maps cover full rows only)
+    if constexpr (!SC) {
+      // partial last rows of the operands (the maps cover full rows only)
       if (threadIdx.x < 2 * TILE) {
         const int c = threadIdx.x % TILE;
         const bool second = threadIdx.x >= TILE;
         const long long rows = second ? g.rows_in2 : g.rows_in;
         const long long tail = second ? g.tail_in2 : g.tail_in;
-        if (tail > 0 && rows < L1) {
+        if ((PAIR || !second) && tail > 0 && rows < L1) {
           const Op2 &op = second ? a.in2 : a.in;
           const int n2 = c0 + c;
-          const double v = n2 < tail ? static_cast<const double *>(op.ptr)[item * op.item_stride +
-                                                                           rows * a.L2 + n2]
-                                     : 0.0;
-          land[((second ? L1 : 0) + rows) * TILE + c] = v;
+          const long long e = item * op.item_stride + rows * a.L2 + n2;
+          if (cin) {
+            landc[rows * TILE + c] = n2 < tail ? static_cast<const cplx *>(op.ptr)[e]
+                                               : make_double2(0.0, 0.0);
+          } else {
+            land[((second ? L1 : 0) + rows) * TILE + c] =
+                n2 < tail ? static_cast<const double *>(op.ptr)[e] : 0.0;
+          }
         }
       }
       __syncthreads();
@@ -165,13 +177,20 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
       cplx *col = ex + c * CS;
       constexpr int S0 = PL::stride(0);
       cplx tw_cur = make_double2(1.0, 0.0), tw_step = make_double2(1.0, 0.0), wrow = tw_step;
-      if constexpr (!PAIR) {
+      if constexpr (SC) {
         tw_step = tw4(a, (long long)n2 * S0);
         if (a.half) wrow = tw4(a, (long long)n2 * L1);  // W_L2^{n2}
       }
       auto in_load = [&](int, int j, int pos) {
         if constexpr (PAIR) {
           return make_double2(land[pos * TILE + c], land[(L1 + pos) * TILE + c]);
+        } else if constexpr (!SC) {
+          const double sc = a.in.scale;
+          if (cin) {
+            const cplx v = landc[pos * TILE + c];
+            return make_double2(v.x * sc, v.y * sc);
+          }
+          return make_double2(land[pos * TILE + c] * sc, 0.0);
         } else {
           cplx v;
           if (a.half && 2 * pos > L1) {
@@ -190,7 +209,7 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
         }
       };
       auto s_store = [&](int, int, int pos, cplx v) { col[fast::swz2(pos)] = v; };
-      fast::pass<PL, 0, false, false, R0, R0>(tp, a.ctw, tw0, in_load, s_store);
+      fast::pass<PL, 0, INV, false, R0, R0>(tp, a.ctw, tw0, in_load, s_store);
     }
     __syncthreads();
     // the landing buffer is consumed: stream the next tile in behind the math
@@ -207,14 +226,17 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
     auto r_store = [&](int i, int j, int, cplx x) { v[i * RL + j] = x; };
     sfor<PL::P - 2>([&](auto qc) {
       constexpr int q = decltype(qc)::value + 1;
-      fast::pass<PL, q, false, false, PL::radix[q], PL::radix[q], L1, true>(t, a.ctw, tw0, s_load,
-                                                                           s_store);
+      fast::pass<PL, q, INV, false, PL::radix[q], PL::radix[q], L1, true>(t, a.ctw, tw0, s_load,
+                                                                         s_store);
       __syncthreads();
     });
-    fast::pass<PL, PL::P - 1, false, false, RL, RL, L1, true>(t, a.ctw, tw0, s_load, r_store);
+    fast::pass<PL, PL::P - 1, INV, false, RL, RL, L1, true>(t, a.ctw, tw0, s_load, r_store);
     __syncthreads();
     // digit-reversed registers -> natural order: register j of butterfly beta
-    // holds frequency k = k(beta) + j * L1 / RL
+    // holds frequency k = k(beta) + j * L1 / RL; single-operand stage A also
+    // applies the four-step twiddle W_L^{-+n2 k} (geometric in j)
+    constexpr bool TW_A = !PAIR && !SC;
+    const cplx tws = TW_A ? tw4(a, (long long)n2 * (L1 / RL)) : make_double2(1.0, 0.0);
 #pragma unroll
     for (int i = 0; i < V / RL; ++i) {
       const int beta = t + i * T;
@@ -225,8 +247,16 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
         k0 += (((beta * RL) / Sp) % Rp) * mul;
         mul *= Rp;
       });
+      cplx cur = TW_A ? tw4(a, (long long)n2 * k0) : make_double2(1.0, 0.0);
 #pragma unroll
-      for (int j = 0; j < RL; ++j) col[k0 + j * (L1 / RL)] = v[i * RL + j];
+      for (int j = 0; j < RL; ++j) {
+        cplx x = v[i * RL + j];
+        if constexpr (TW_A) {
+          x = INV ? cmulc(x, cur) : cmul(x, cur);
+          cur = cmul(cur, tws);
+        }
+        col[k0 + j * (L1 / RL)] = x;
+      }
     }
     __syncthreads();
     if constexpr (PAIR) {
@@ -276,6 +306,14 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
       }
       __syncthreads();
       store_rows(a.out2);
+    } else if constexpr (!SC) {
+      const Out2 &o = a.out;
+      const int rows = o.e1 < L1 ? o.e1 : L1;
+      cplx *dst = static_cast<cplx *>(o.ptr) + item * o.item_stride + c0;
+      for (int idx = threadIdx.x; idx < TILE * rows; idx += NT) {
+        const int cc = idx % TILE, r = idx / TILE;
+        if (c0 + cc < o.e2) dst[r * o.s1 + cc] = ex[cc * CS + r];
+      }
     } else {
       // y(m2 + L2 k) for the rows k with m2 + L2 k < len
       const Out2 &o = a.out;
@@ -348,36 +386,42 @@ static cudaError_t launch_t(const ColTma &g, long long items, int ncols, cudaStr
 
 }  // namespace large
 
-// cudaErrorNotSupported unless the request is a 1D four-step column pass this
-// kernel implements (L1 = 1536, contiguous rows of length L2, f64 operands for
-// the packed pass, complex Q for the final pass).
-cudaError_t launch_cols_tma(int stage, const large::ColArgs &a, long long items, int ncols,
-                            cudaStream_t stream) {
-  using namespace large;
-  if (getenv("HK_NO_COLTMA")) return cudaErrorNotSupported;
-  if (!a.twiddle || a.L1 != 1536 || items > 65535) return cudaErrorNotSupported;
-  constexpr int TILE = 4;
-  using PL = Plan1D<1536, 96, 6, 16, 16>;
+namespace large {
+template <class PL, int TILE>
+static cudaError_t launch_cols_tma_t(int stage, const ColArgs &a, long long items, int ncols,
+                                     cudaStream_t stream) {
   ColTma g{};
   g.a = a;
   const long long L2 = a.L2;
+  auto full_rows = [&](const Op2 &op, long long *rows, long long *tail) {
+    *rows = std::min<long long>(a.L1, op.len / L2);
+    *tail = op.len - *rows * L2;
+    return *rows > 0 && *tail < L2;
+  };
   if (stage == ST_A_PAIR) {
     const Op2 &h = a.in, &x = a.in2;
     if (h.kind != FK_F64 || x.kind != FK_F64 || h.s1 != L2 || h.s2 != 1 || x.s1 != L2 ||
         x.s2 != 1 || h.len < 0 || x.len < 0 || a.out.s2 != 1 || a.out2.s2 != 1)
       return cudaErrorNotSupported;
-    g.rows_in = std::min<long long>(a.L1, h.len / L2);
-    g.tail_in = h.len - g.rows_in * L2;
-    g.rows_in2 = std::min<long long>(a.L1, x.len / L2);
-    g.tail_in2 = x.len - g.rows_in2 * L2;
-    if (g.tail_in >= L2 || g.tail_in2 >= L2) return cudaErrorNotSupported;
-    if (!encode(&g.m_in, h.ptr, L2, std::max<long long>(g.rows_in, 1), items, L2, h.item_stride,
-                TILE) ||
-        !encode(&g.m_in2, x.ptr, L2, std::max<long long>(g.rows_in2, 1), items, L2,
-                x.item_stride, TILE))
+    if (!full_rows(h, &g.rows_in, &g.tail_in) || !full_rows(x, &g.rows_in2, &g.tail_in2))
       return cudaErrorNotSupported;
-    if (g.rows_in == 0 || g.rows_in2 == 0) return cudaErrorNotSupported;
+    if (!encode(&g.m_in, h.ptr, L2, g.rows_in, items, L2, h.item_stride, TILE) ||
+        !encode(&g.m_in2, x.ptr, L2, g.rows_in2, items, L2, x.item_stride, TILE))
+      return cudaErrorNotSupported;
     return launch_t<PL, TILE, ST_A_PAIR>(g, items, ncols, stream);
+  }
+  if (stage == ST_A_FWD || stage == ST_A_INV) {
+    const Op2 &op = a.in;
+    const bool cx = op.kind == FK_C128;
+    if ((!cx && op.kind != FK_F64) || op.s1 != L2 || op.s2 != 1 || op.len < 0 || a.out.s2 != 1 ||
+        a.out.len >= 0 || a.in_n1_fast)
+      return cudaErrorNotSupported;
+    if (!full_rows(op, &g.rows_in, &g.tail_in)) return cudaErrorNotSupported;
+    const int f = cx ? 2 : 1;
+    if (!encode(&g.m_in, op.ptr, f * L2, g.rows_in, items, f * L2, f * op.item_stride, f * TILE))
+      return cudaErrorNotSupported;
+    return stage == ST_A_FWD ? launch_t<PL, TILE, ST_A_FWD>(g, items, ncols, stream)
+                             : launch_t<PL, TILE, ST_A_INV>(g, items, ncols, stream);
   }
   if (stage == ST_C) {
     const Op2 &q = a.in;
@@ -390,6 +434,23 @@ cudaError_t launch_cols_tma(int stage, const large::ColArgs &a, long long items,
     return launch_t<PL, TILE, ST_C>(g, items, ncols, stream);
   }
   return cudaErrorNotSupported;
+}
+}  // namespace large
+
+bool tma_col_len(long long L1) { return L1 == 1536 || L1 == 3072; }
+
+// cudaErrorNotSupported unless the request is a 1D four-step column pass this
+// kernel implements (L1 in {1536, 3072}, contiguous rows of length L2).
+cudaError_t launch_cols_tma(int stage, const large::ColArgs &a, long long items, int ncols,
+                            cudaStream_t stream) {
+  using namespace large;
+  if (getenv("HK_NO_COLTMA")) return cudaErrorNotSupported;
+  if (!a.twiddle || items > 65535) return cudaErrorNotSupported;
+  switch (a.L1) {
+    case 1536: return launch_cols_tma_t<Plan1D<1536, 96, 6, 16, 16>, 4>(stage, a, items, ncols, stream);
+    case 3072: return launch_cols_tma_t<Plan1D<3072, 192, 12, 16, 16>, 2>(stage, a, items, ncols, stream);
+    default: return cudaErrorNotSupported;
+  }
 }
 
 }  // namespace hk

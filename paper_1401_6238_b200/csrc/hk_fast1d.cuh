@@ -135,6 +135,14 @@ __global__ void __launch_bounds__(PL::CTA, (min_blocks_for<PL, STG>()))
   else
     tw0 = Tw0Global{a.tw0, PL::L / PL::radix[0], PL::radix[0]};
   const GroupSync<PL> gsync;
+  // one product per CTA with several pass-0 butterflies per thread (8192):
+  // issue all of a thread's operand loads before its butterflies
+  auto hoist_if_big = [](auto f) {
+    if constexpr (PL::T >= 512)
+      return Hoisted<decltype(f)>{f};
+    else
+      return f;
+  };
   const bool do_pf = a.prefetch != 0;
   if (do_pf && threadIdx.x == 0) prefetch_block(a, blockIdx.x, PL::G);
 
@@ -229,7 +237,8 @@ __global__ void __launch_bounds__(PL::CTA, (min_blocks_for<PL, STG>()))
       } else {
         const double sc = a.scale;
         fft_dif<PL, true, PL::radix[0], PL::L, kRec>(
-            sbuf, t, tw, tw0, [&](int pos) { return load_elem(hf, off, pos, sc); }, v, gsync);
+            sbuf, t, tw, tw0, hoist_if_big([&](int pos) { return load_elem(hf, off, pos, sc); }),
+            v, gsync);
       }
       if (a.mode == M_SPEC_H) {
         if (active) {
@@ -261,8 +270,9 @@ __global__ void __launch_bounds__(PL::CTA, (min_blocks_for<PL, STG>()))
               cpa_commit();
             });
       } else {
-        fft_dif<PL, false, NZ, PL::L, kRec>(sbuf, t, tw, tw0,
-                               [&](int pos) { return load_elem(fa, off, pos, 1.0); }, v, gsync);
+        fft_dif<PL, false, NZ, PL::L, kRec>(
+            sbuf, t, tw, tw0, hoist_if_big([&](int pos) { return load_elem(fa, off, pos, 1.0); }),
+            v, gsync);
       }
       tmem_wait_st();
 #pragma unroll

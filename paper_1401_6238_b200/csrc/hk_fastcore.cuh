@@ -177,7 +177,7 @@ struct Tw0Global {
 // shared-memory carve-out (the strided reads of a W_L table touch one 128-B
 // line per twiddle).
 template <class PL, int p, bool INV, bool FINAL, int NZ, int NO, int TWL = PL::L, bool REC = false,
-          class TW0, class Load, class Store, class C, class PreStore = NoHookT>
+          class TW0, class Load, class Store, class C, class PreStore = NoHookT, bool HOIST = false>
 __device__ __forceinline__ void pass(int t, const C *__restrict__ tw, const TW0 &tw0,
                                      Load &&load, Store &&store, PreStore pre_store = PreStore()) {
   using Tr = Traits<PL>;
@@ -198,6 +198,31 @@ __device__ __forceinline__ void pass(int t, const C *__restrict__ tw, const TW0 
   // so one table read serves all NB butterflies (8192 = 2 x 16^3: NB = 8).
   [[maybe_unused]] C base0 = CT<C>::make(1, 0);
   if constexpr (p == 0 && PL::P > 1 && NB > 1 && is_tw0rec<TW0>::value) base0 = tw0.base(t);
+  // HOIST: issue every load of the thread's NB butterflies before the first
+  // butterfly (global operands: one exposed latency per pass, not NB)
+  constexpr bool kHoist = HOIST && !std::is_same_v<std::decay_t<Load>, SmemIO>;
+  [[maybe_unused]] C pre[kHoist ? NB : 1][kHoist ? NIN : 1];
+  if constexpr (kHoist) {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const int beta = t + i * PL::T;
+      if (NBUT % PL::T == 0 || beta < NBUT) {
+        int lo, hi;
+        if constexpr (HIM) {
+          hi = beta % H;
+          lo = beta / H;
+        } else {
+          lo = beta % s;
+          hi = beta / s;
+        }
+        const int base = hi * Lp + lo;
+        sfor<NIN>([&](auto jc) {
+          constexpr int j = decltype(jc)::value;
+          pre[i][j] = load(i, j, base + j * s);
+        });
+      }
+    }
+  }
 #pragma unroll
   for (int i = 0; i < NB; ++i) {
     const int beta = t + i * PL::T;
@@ -219,6 +244,8 @@ __device__ __forceinline__ void pass(int t, const C *__restrict__ tw, const TW0 
           constexpr int j = decltype(jc)::value;
           a[j] = ad.template ld<j>();
         });
+      } else if constexpr (kHoist) {
+        sfor<NIN>([&](auto jc) { a[decltype(jc)::value] = pre[i][decltype(jc)::value]; });
       } else {
         sfor<NIN>([&](auto jc) {
           constexpr int j = decltype(jc)::value;
@@ -338,6 +365,17 @@ struct NoHook {
 // Entry object is called instead right before the pass-0 stores (a split
 // arrive/wait barrier whose wait then overlaps the pass-0 loads and math).
 struct SyncEntry {};
+// A global-operand loader wrapped in Hoisted makes fft_dif's first pass issue
+// all of a thread's loads before its butterflies (fast::pass HOIST).
+template <class F>
+struct Hoisted {
+  F f;
+  __device__ __forceinline__ auto operator()(int pos) const { return f(pos); }
+};
+template <class T>
+struct IsHoisted : std::false_type {};
+template <class F>
+struct IsHoisted<Hoisted<F>> : std::true_type {};
 
 // hook() runs (on every thread) right after the barrier that follows pass 0,
 // i.e. once every thread of the group has consumed the pass-0 input.
@@ -354,6 +392,7 @@ __device__ __forceinline__ void fft_dif(C *sbuf, int t, const C *__restrict__ tw
                                         Sync sync = Sync(), Hook hook = Hook(),
                                         WSync * = nullptr, Entry entry = Entry()) {
   constexpr bool kEntrySync = std::is_same_v<Entry, SyncEntry>;
+  constexpr bool kHoistG = IsHoisted<std::decay_t<GLoad>>::value;
   auto last_sync = [&]() {
     if constexpr (std::is_void_v<WSync>)
       sync();
@@ -380,8 +419,8 @@ __device__ __forceinline__ void fft_dif(C *sbuf, int t, const C *__restrict__ tw
   using SL = decltype(s_load);
   using SS = decltype(s_store);
   if constexpr (kEntrySync)
-    pass<PL, 0, INV, false, (NZ < R0 ? NZ : R0), R0, TWL, REC, TW0, decltype(g_load) &, SS>(
-        t, tw, tw0, g_load, s_store);
+    pass<PL, 0, INV, false, (NZ < R0 ? NZ : R0), R0, TWL, REC, TW0, decltype(g_load) &, SS, C,
+         NoHookT, kHoistG>(t, tw, tw0, g_load, s_store);
   else
     pass<PL, 0, INV, false, (NZ < R0 ? NZ : R0), R0, TWL, REC, TW0, decltype(g_load) &, SS, C,
          Entry &>(t, tw, tw0, g_load, s_store, entry);

@@ -56,6 +56,7 @@ struct ColArgs {
 }  // namespace large
 
 bool supported_col_len(long long L1);
+bool tma_col_len(long long L1);  // column lengths of the TMA column kernel
 cudaError_t launch_cols(int stage, const large::ColArgs &a, long long items, int ncols,
                         cudaStream_t stream);
 // TMA-fed column passes (hk_cols_tma.cu); cudaErrorNotSupported outside their shapes

@@ -80,6 +80,15 @@ __device__ __forceinline__ void war_arrive(uint32_t addr) {
   if ((threadIdx.x & 31) == 0) mbar_arrive(addr);
 }
 
+// Named barrier with a runtime id (one code copy serves both groups).
+template <int N>
+struct GroupBar {
+  int id;
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "n"(N) : "memory");
+  }
+};
+
 template <int ID, int N>
 struct NamedSync {
   __device__ __forceinline__ void operator()() const {
@@ -119,12 +128,28 @@ struct Layout {
 // TWV bit 0: pass-0 twiddles by recurrence from W_L^t (else the TMEM slab);
 // bit 1: pass->=1 twiddles by recurrence from one compact-table read;
 // bit 3: pass-1 twiddles from TMEM too (slabs shared by the two groups).
+// Product k of a CTA is item b = blockIdx.x + k * gridDim.x of the batch, at
+// operand offset (b / nsub) * bstride + (b % nsub) * sstride (the two-level
+// row stage runs nsub rows per item; plain batches have nsub = 1).
+template <bool ROWS>
+__device__ __forceinline__ long long pp_off(const Args1D &a, long long b, long long bs,
+                                            long long ss) {
+  if (!ROWS || a.nsub == 1) return b * bs;  // plain batches launch with nsub == 1
+  const long long ob = b / a.nsub;
+  return ob * bs + (b - ob * a.nsub) * ss;
+}
+
+// XD (NZ == R0: x is a full-length row, the two-level row stage): x is not
+// staged in shared memory (it would not fit next to three L buffers); pass 0
+// of fft(x) issues all of a thread's global loads up front, the rows are
+// prefetched into L2 one product ahead, and the other group covers the wait.
 template <class PL, int NZ, int NO, int TWV>
 __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constant__ Args1D a) {
   constexpr bool REC = (TWV & 2) != 0;
   constexpr int L = PL::L, T = PL::T, V = PL::V, R0 = PL::radix[0];
   constexpr int S0 = PL::stride(0);
-  constexpr int XS = NZ * S0;  // staged x elements
+  constexpr bool XD = NZ >= R0;
+  constexpr int XS = XD ? 0 : NZ * S0;  // staged x elements
   constexpr int TW1 = L / R0;  // passes >= 1 read the compact W_{L/R0} table
   (void)Layout<PL>{};
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -146,7 +171,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
   // The TMA only ever writes the first h.len (x.len) staged elements: zero the
   // tails once so the first passes read the zero padding without bounds tests.
   for (int i = a.h.len + (int)threadIdx.x; i < L; i += blockDim.x) hst[i] = make_double2(0.0, 0.0);
-  for (int i = a.fac[0].len + (int)threadIdx.x; i < XS; i += blockDim.x) {
+  for (int i = (XD ? XS : a.fac[0].len) + (int)threadIdx.x; i < XS; i += blockDim.x) {
     xst[i] = make_double2(0.0, 0.0);
     xst[XS + i] = make_double2(0.0, 0.0);
   }
@@ -227,22 +252,38 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
   const long long nloc = a.batch > blockIdx.x
                              ? (a.batch - blockIdx.x + gridDim.x - 1) / gridDim.x
                              : 0;
+  auto hptr = [&](long long k) {
+    return static_cast<const cplx *>(a.h.ptr) +
+           pp_off<XD>(a, blockIdx.x + k * gridDim.x, a.h.bstride, a.h.sstride);
+  };
+  auto xptr = [&](long long k) {
+    return static_cast<const cplx *>(a.fac[0].ptr) +
+           pp_off<XD>(a, blockIdx.x + k * gridDim.x, a.fac[0].bstride, a.fac[0].sstride);
+  };
+  auto x_prefetch = [&](long long k) {  // XD: row k of this CTA into L2
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(xptr(k)),
+                 "r"((unsigned)a.fac[0].len * 16u)
+                 : "memory");
+  };
   if (threadIdx.x == 0) {
     const uint32_t hbytes = (uint32_t)a.h.len * 16u, xbytes = (uint32_t)a.fac[0].len * 16u;
     if (nloc > 0) {
       mbar_expect_tx(mb_h0, hbytes);
-      tma_load(smem_u32(hst), static_cast<const cplx *>(a.h.ptr) + blockIdx.x * a.h.bstride,
-               hbytes, mb_h0);
-      mbar_expect_tx(mb_x0, xbytes);
-      tma_load(smem_u32(xst),
-               static_cast<const cplx *>(a.fac[0].ptr) + blockIdx.x * a.fac[0].bstride, xbytes,
-               mb_x0);
+      tma_load(smem_u32(hst), hptr(0), hbytes, mb_h0);
+      if constexpr (XD) {
+        x_prefetch(0);
+      } else {
+        mbar_expect_tx(mb_x0, xbytes);
+        tma_load(smem_u32(xst), xptr(0), xbytes, mb_x0);
+      }
     }
     if (nloc > 1) {
-      mbar_expect_tx(mb_x0 + 8, xbytes);
-      tma_load(smem_u32(xst + XS),
-               static_cast<const cplx *>(a.fac[0].ptr) + (blockIdx.x + gridDim.x) * a.fac[0].bstride,
-               xbytes, mb_x0 + 8);
+      if constexpr (XD) {
+        x_prefetch(1);
+      } else {
+        mbar_expect_tx(mb_x0 + 8, xbytes);
+        tma_load(smem_u32(xst + XS), xptr(1), xbytes, mb_x0 + 8);
+      }
     }
   }
 
@@ -255,8 +296,11 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
   // transforms) become split mbarrier arrive/wait pairs
   constexpr bool SPLIT = TW1T && (TWV & 16) != 0;
   using Entry = std::conditional_t<SPLIT, WarWait, fast::SyncEntry>;
+  // TWV bit 5: both groups run ONE copy of the loop (runtime group index):
+  // half the instruction footprint of the two compile-time copies
   auto run = [&](auto gc) {
-    constexpr int G = decltype(gc)::value;
+    constexpr bool RT = (TWV & 32) != 0;
+    const int G = RT ? g : decltype(gc)::value;
     auto h_entry = [&](int kk) {
       if constexpr (SPLIT)
         return Entry{mb_wh0 + 8 * G, (uint32_t)((kk - 1) & 1), kk > 0};
@@ -269,7 +313,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
       else
         return Entry{};
     };
-    const NamedSync<1 + G, T> sync;
+    const GroupBar<T> sync{1 + G};
     cplx *sbuf = ex + G * L;
     cplx *my_x = xst + G * XS;
     int kk = 0;
@@ -295,10 +339,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
               const uint32_t bytes = (uint32_t)a.h.len * 16u;
               fence_proxy_async();
               mbar_expect_tx(mb, bytes);
-              tma_load(smem_u32(hst),
-                       static_cast<const cplx *>(a.h.ptr) +
-                           (blockIdx.x + (k + 1) * gridDim.x) * a.h.bstride,
-                       bytes, mb);
+              tma_load(smem_u32(hst), hptr(k + 1), bytes, mb);
             }
           },
           (WS *)nullptr, h_entry(kk));
@@ -307,23 +348,34 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
 #pragma unroll
       for (int c = 0; c < V / 4; ++c) tmem_st4(tacc + 16 * c, &v[4 * c]);
       // ---- X = fft(x~) from staged x; refill this group's xst with product k+2
-      mbar_wait(mb_x0 + 8 * G, par);
       t = fresh_t();
-      fast::fft_dif<PL, false, NZ, TW1, REC>(
-          sbuf, t, a.tw1, tw0, [&](int pos) { return my_x[pos]; }, v,
-          sync, [&]() {
-            if (t == 0 && k + 2 < nloc) {
-              const uint32_t mb = mb_x0 + 8 * G;
-              const uint32_t bytes = (uint32_t)a.fac[0].len * 16u;
-              fence_proxy_async();
-              mbar_expect_tx(mb, bytes);
-              tma_load(smem_u32(my_x),
-                       static_cast<const cplx *>(a.fac[0].ptr) +
-                           (blockIdx.x + (k + 2) * gridDim.x) * a.fac[0].bstride,
-                       bytes, mb);
-            }
-          },
-          (WS *)nullptr, x_entry(kk));
+      if constexpr (XD) {
+        const cplx *xp = xptr(k);
+        const int xlen = a.fac[0].len;
+        auto xl = [xp, xlen](int pos) {
+          return pos < xlen ? fast::ld_stream(xp + pos) : make_double2(0.0, 0.0);
+        };
+        fast::fft_dif<PL, false, NZ, TW1, REC>(
+            sbuf, t, a.tw1, tw0, fast::Hoisted<decltype(xl)>{xl}, v, sync,
+            [&]() {
+              if (t == 0 && k + 2 < nloc) x_prefetch(k + 2);
+            },
+            (WS *)nullptr, x_entry(kk));
+      } else {
+        mbar_wait(mb_x0 + 8 * G, par);
+        fast::fft_dif<PL, false, NZ, TW1, REC>(
+            sbuf, t, a.tw1, tw0, [&](int pos) { return my_x[pos]; }, v,
+            sync, [&]() {
+              if (t == 0 && k + 2 < nloc) {
+                const uint32_t mb = mb_x0 + 8 * G;
+                const uint32_t bytes = (uint32_t)a.fac[0].len * 16u;
+                fence_proxy_async();
+                mbar_expect_tx(mb, bytes);
+                tma_load(smem_u32(my_x), xptr(k + 2), bytes, mb);
+              }
+            },
+            (WS *)nullptr, x_entry(kk));
+      }
       tmem_wait_st();
 #pragma unroll
       for (int c = 0; c < V / 4; ++c) {
@@ -338,21 +390,25 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
       }
       // ---- y = fft(acc)[:n_1]
       t = fresh_t();
+      cplx *yk = static_cast<cplx *>(a.out) +
+                 pp_off<XD>(a, blockIdx.x + k * gridDim.x, a.out_bstride, a.out_sstride);
       fast::fft_final<PL, NO, TW1, REC>(
           sbuf, t, a.tw1, tw0, v,
           [&](int pos, cplx val) {
-            if (pos < a.out_len)
-              static_cast<cplx *>(a.out)[(blockIdx.x + k * gridDim.x) * a.out_bstride + pos] =
-                  make_double2(val.x * a.scale, val.y * a.scale);
+            if (pos < a.out_len) yk[pos] = make_double2(val.x * a.scale, val.y * a.scale);
           },
           sync, (WS *)nullptr);
       if constexpr (SPLIT) war_arrive(mb_wh0 + 8 * G);
     }
   };
-  if (g == 0)
+  if constexpr ((TWV & 32) != 0) {
     run(std::integral_constant<int, 0>{});
-  else
-    run(std::integral_constant<int, 1>{});
+  } else {
+    if (g == 0)
+      run(std::integral_constant<int, 0>{});
+    else
+      run(std::integral_constant<int, 1>{});
+  }
 
   tmem_fence_before();
   __syncthreads();
@@ -364,7 +420,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
 
 template <class PL, int NZ, int NO, int TWV>
 static cudaError_t launch_pp(const Args1D &a, cudaStream_t stream) {
-  constexpr int XS = NZ * PL::stride(0);
+  constexpr int XS = NZ >= PL::radix[0] ? 0 : NZ * PL::stride(0);
   const int smem = (3 * PL::L + 2 * XS) * (int)sizeof(cplx) + 128;
   static std::atomic<unsigned long long> configured{0};
   static int sms[64] = {0};
@@ -392,7 +448,7 @@ static cudaError_t launch_pp(const Args1D &a, cudaStream_t stream) {
 // batched H x^{m-1} shape it implements.
 cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream) {
   if (getenv("HK_NO_PP")) return cudaErrorNotSupported;
-  if (L != 4096 || a.mode != M_PARTIAL || a.nfac != 1 || !a.tw0 || a.nsub != 1)
+  if (L != 4096 || a.mode != M_PARTIAL || a.nfac != 1 || !a.tw0 || a.nsub < 1 || a.ncombo)
     return cudaErrorNotSupported;
   const Factor &h = a.h, &x = a.fac[0];
   if (h.kind != FK_C128 || x.kind != FK_C128 || h.estride != 1 || x.estride != 1 ||
@@ -407,11 +463,17 @@ cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream) {
   // 24: TMEM pass-0 and pass-1 twiddles + split WAR barriers (r02: 169.4 us vs
   // 170.0 for 8 and 185.6 for 2 = recurrence for pass 1, the r01 default)
   int twv = 24;
-  if (const char *e = getenv("HK_PP_TWV")) twv = atoi(e) & 31;
-  if (nz <= 4 && no <= 4) {
+  if (const char *e = getenv("HK_PP_TWV")) twv = atoi(e) & 63;
+  if (nz == 16 && !getenv("HK_NO_PP_ROWS")) {  // full rows (two-level row stage)
+    const bool one = getenv("HK_PP_ROWS_TWO") == nullptr;  // A/B: two code copies
+    if (no <= 4) return one ? pp::launch_pp<PL, 16, 4, 56>(a, stream) : pp::launch_pp<PL, 16, 4, 24>(a, stream);
+    return one ? pp::launch_pp<PL, 16, 16, 56>(a, stream) : pp::launch_pp<PL, 16, 16, 24>(a, stream);
+  }
+  if (nz <= 4 && no <= 4 && a.nsub == 1) {
     switch (twv) {
       case 8: return pp::launch_pp<PL, 4, 4, 8>(a, stream);
       case 24: return pp::launch_pp<PL, 4, 4, 24>(a, stream);
+      case 56: return pp::launch_pp<PL, 4, 4, 56>(a, stream);
       case 6: return pp::launch_pp<PL, 4, 4, 6>(a, stream);
       case 1: return pp::launch_pp<PL, 4, 4, 1>(a, stream);
       case 2: return pp::launch_pp<PL, 4, 4, 2>(a, stream);
