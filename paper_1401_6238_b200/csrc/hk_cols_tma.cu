@@ -34,11 +34,16 @@ namespace hk {
 namespace large {
 
 struct alignas(64) ColTma {
-  CUtensorMap m_in;   // ST_A_PAIR: h (f64 [items][rows][L2]); ST_C: Q (f64 pairs)
-  CUtensorMap m_in2;  // ST_A_PAIR: x
+  CUtensorMap m_in;    // ST_A_PAIR: h (f64 [items][rows][L2]); ST_C: Q (f64 pairs)
+  CUtensorMap m_in2;   // ST_A_PAIR: x
+  CUtensorMap m_out;   // tma_out: stage-A output of h (or of the operand) / y
+  CUtensorMap m_out2;  // tma_out, ST_A_PAIR: stage-A output of x
   ColArgs a;
   long long rows_in, rows_in2;  // full rows the maps cover (TMA zero-fills below)
   long long tail_in, tail_in2;  // valid elements of the partial row after them
+  int32_t tma_out;              // 1: epilogue stores the tile with TMA (row-major staging)
+  int32_t out_rows;             // rows of the output tile (stage A: e1; ST_C: len / L2)
+  int32_t nat_swz;              // natural-order column layout: k ^ ((k >> 3) & nat_swz)
 };
 
 namespace tma {
@@ -72,6 +77,18 @@ __device__ __forceinline__ void load3d(uint32_t dst, const CUtensorMap *map, int
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
+__device__ __forceinline__ void store3d(const CUtensorMap *map, int c0, int c1, int c2, uint32_t src) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(src)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
 }  // namespace tma
 
@@ -89,7 +106,12 @@ struct TmaLayout {
   static constexpr bool PAIR = STAGE == ST_A_PAIR;
   // ST_C lands at most L1 complex rows (all of them without `half`)
   static constexpr int LAND = PAIR ? 2 * L1 * TILE * 8 : L1 * TILE * 16;
-  static constexpr int EX = TILE * CS * 16;
+  // TMA-store epilogue of the Hermitian pair: H rows [0, R), X rows from XOFF
+  // (128-byte aligned), row-major [row][TILE] in the exchange buffer
+  static constexpr int R = L1 / 2 + 1;
+  static constexpr int XOFF = (R + (8 / TILE) - 1) / (8 / TILE) * (8 / TILE);
+  static constexpr int EX0 = TILE * CS * 16, EX1 = (XOFF + R) * TILE * 16;
+  static constexpr int EX = EX0 > EX1 ? EX0 : EX1;
   static constexpr int SMEM = LAND + EX + 128;
   static_assert(L1 % BR == 0, "column length must be a multiple of the box height");
 };
@@ -148,6 +170,10 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
     const long long item = w / tiles_per_item;
     const int c0 = (int)(w - item * tiles_per_item) * TILE;
     tma::mbar_wait(mb, (uint32_t)(it & 1));
+    if (g.tma_out) {  // the previous tile's TMA stores have read the exchange buffer
+      if (threadIdx.x == 0) tma::bulk_wait_read();
+      if constexpr (SC) __syncthreads();
+    }
     if constexpr (!SC) {
       // partial last rows of the operands (the maps cover full rows only)
       if (threadIdx.x < 2 * TILE) {
@@ -235,6 +261,10 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
     // digit-reversed registers -> natural order: register j of butterfly beta
     // holds frequency k = k(beta) + j * L1 / RL; single-operand stage A also
     // applies the four-step twiddle W_L^{-+n2 k} (geometric in j)
+    // natural-order positions are XOR-swizzled (bank conflicts of the
+    // digit-reversed writes at L1 = 3072: 8 wavefronts per warp store -> 4)
+    const int nswz = g.nat_swz;
+    auto nat = [nswz](int k) { return k ^ ((k >> 3) & nswz); };
     constexpr bool TW_A = !PAIR && !SC;
     const cplx tws = TW_A ? tw4(a, (long long)n2 * (L1 / RL)) : make_double2(1.0, 0.0);
 #pragma unroll
@@ -255,10 +285,59 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
           x = INV ? cmulc(x, cur) : cmul(x, cur);
           cur = cmul(cur, tws);
         }
-        col[k0 + j * (L1 / RL)] = x;
+        const int k = k0 + j * (L1 / RL);
+        if (g.tma_out)
+          ex[k * TILE + c] = x;  // row-major staging for the TMA store
+        else
+          col[nat(k)] = x;
       }
     }
     __syncthreads();
+    if (g.tma_out) {
+      // ---- TMA-store epilogue
+      if constexpr (PAIR) {
+        constexpr int R = LY::R, XO = LY::XOFF, NP = (R + T - 1) / T;
+        cplx za[NP], zb[NP];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const int k = t + p * T;
+          if (k < R) {
+            za[p] = ex[k * TILE + c];
+            zb[p] = ex[(k == 0 ? 0 : L1 - k) * TILE + c];
+          }
+        }
+        __syncthreads();
+        const double sh = a.in.scale;
+        cplx wk = tw4(a, (long long)n2 * t);
+        const cplx wstep = tw4(a, (long long)n2 * T);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const int k = t + p * T;
+          if (k < R) {
+            const cplx A = za[p], B = zb[p];
+            const cplx H = make_double2(0.5 * (A.x + B.x), 0.5 * (A.y - B.y));
+            const cplx X = make_double2(0.5 * (A.y + B.y), 0.5 * (B.x - A.x));
+            const cplx hk = cmul(H, wk), xk = cmul(X, wk);
+            ex[k * TILE + c] = make_double2(hk.x * sh, -hk.y * sh);
+            ex[(XO + k) * TILE + c] = xk;
+          }
+          wk = cmul(wk, wstep);
+        }
+      }
+      tma::fence_proxy_async();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int rows = g.out_rows;
+        const int inner = 2 * c0;
+        for (int r0 = 0; r0 < rows; r0 += BR) {
+          tma::store3d(&g.m_out, inner, r0, (int)item, smem_u32(ex + r0 * TILE));
+          if constexpr (PAIR)
+            tma::store3d(&g.m_out2, inner, r0, (int)item, smem_u32(ex + (LY::XOFF + r0) * TILE));
+        }
+        tma::bulk_commit();
+      }
+      continue;  // the next tile waits for these reads before reusing ex
+    }
     if constexpr (PAIR) {
       // Z(k) = H(k) + i X(k):  H(k) = (Z(k) + conj Z(-k)) / 2,
       // X(k) = (Z(k) - conj Z(-k)) / 2i; h takes the inverse (conj H, 1/L)
@@ -274,26 +353,31 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
         const int k = t + p * T;
         if (k <= L1 / 2) {
           const int kk = k == 0 ? 0 : L1 - k;
-          const cplx A = col[k], B = col[kk];
+          const cplx A = col[nat(k)], B = col[nat(kk)];
           const cplx H = make_double2(0.5 * (A.x + B.x), 0.5 * (A.y - B.y));
           const cplx X = make_double2(0.5 * (A.y + B.y), 0.5 * (B.x - A.x));
           const cplx wkk = k == 0 ? wk : cmulc(wl1, wk);
           const cplx hk = cmul(H, wk), hkk = cmulc(H, wkk);
           xa[p] = cmul(X, wk);
           xb[p] = cmul(make_double2(X.x, -X.y), wkk);
-          col[k] = make_double2(hk.x * sh, -hk.y * sh);
-          if (kk != k) col[kk] = make_double2(hkk.x * sh, hkk.y * sh);
+          col[nat(k)] = make_double2(hk.x * sh, -hk.y * sh);
+          if (kk != k) col[nat(kk)] = make_double2(hkk.x * sh, hkk.y * sh);
         }
         wk = cmul(wk, wstep);
       }
       __syncthreads();
       const int rows_out = a.out.e1;  // L1/2 + 1 with `half`, else L1
+      // thread -> fixed column cc = tid % TILE, rows r0, r0 + NT/TILE, ...
       auto store_rows = [&](const Out2 &o) {
-        cplx *dst = static_cast<cplx *>(o.ptr) + item * o.item_stride + c0;
-        for (int idx = threadIdx.x; idx < TILE * rows_out; idx += NT) {
-          const int cc = idx % TILE, r = idx / TILE;
-          if (c0 + cc < a.L2) dst[r * o.s1 + cc] = ex[cc * CS + r];
-        }
+        const int cc = threadIdx.x % TILE;
+        if (c0 + cc >= a.L2) return;
+        constexpr int RS = NT / TILE;
+        const cplx *src = ex + cc * CS;
+        cplx *d = static_cast<cplx *>(o.ptr) + item * o.item_stride + c0 + cc;
+        const long long step = (long long)RS * o.s1;
+        int r = threadIdx.x / TILE;
+        d += r * o.s1;
+        for (; r < rows_out; r += RS, d += step) *d = src[nat(r)];
       };
       store_rows(a.out);
       __syncthreads();
@@ -301,32 +385,40 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
       for (int p = 0; p < NP; ++p) {
         const int k = t + p * T;
         if (k > L1 / 2) continue;
-        col[k] = xa[p];
-        if (k != 0 && 2 * k != L1) col[L1 - k] = xb[p];
+        col[nat(k)] = xa[p];
+        if (k != 0 && 2 * k != L1) col[nat(L1 - k)] = xb[p];
       }
       __syncthreads();
       store_rows(a.out2);
     } else if constexpr (!SC) {
       const Out2 &o = a.out;
       const int rows = o.e1 < L1 ? o.e1 : L1;
-      cplx *dst = static_cast<cplx *>(o.ptr) + item * o.item_stride + c0;
-      for (int idx = threadIdx.x; idx < TILE * rows; idx += NT) {
-        const int cc = idx % TILE, r = idx / TILE;
-        if (c0 + cc < o.e2) dst[r * o.s1 + cc] = ex[cc * CS + r];
+      const int cc = threadIdx.x % TILE;
+      if (c0 + cc < o.e2) {
+        constexpr int RS = NT / TILE;
+        const cplx *src = ex + cc * CS;
+        int r = threadIdx.x / TILE;
+        cplx *d = static_cast<cplx *>(o.ptr) + item * o.item_stride + c0 + cc + r * o.s1;
+        for (; r < rows; r += RS, d += (long long)RS * o.s1) *d = src[nat(r)];
       }
     } else {
       // y(m2 + L2 k) for the rows k with m2 + L2 k < len
       const Out2 &o = a.out;
-      const long long krows = (o.len - c0 + a.L2 - 1) / a.L2;
-      const int rows = (int)(krows < L1 ? krows : L1);
-      cplx *dst = static_cast<cplx *>(o.ptr) + item * o.item_stride + c0 * o.s2;
-      for (int idx = threadIdx.x; idx < TILE * rows; idx += NT) {
-        const int cc = idx % TILE, r = idx / TILE;
-        if ((long long)(c0 + cc) + (long long)a.L2 * r < o.len) dst[r * o.s1 + cc * o.s2] = ex[cc * CS + r];
+      const int cc = threadIdx.x % TILE;
+      if (c0 + cc < a.L2) {
+        // rows r with (c0 + cc) + L2 r < len
+        const long long krows = (o.len - (c0 + cc) + a.L2 - 1) / a.L2;
+        const int rows = (int)(krows < L1 ? krows : L1);
+        constexpr int RS = NT / TILE;
+        const cplx *src = ex + cc * CS;
+        int r = threadIdx.x / TILE;
+        cplx *d = static_cast<cplx *>(o.ptr) + item * o.item_stride + (c0 + cc) * o.s2 + r * o.s1;
+        for (; r < rows; r += RS, d += (long long)RS * o.s1) *d = src[nat(r)];
       }
     }
     __syncthreads();  // exchange buffer reused by the next tile's pass 0
   }
+  if (g.tma_out && threadIdx.x == 0) tma::bulk_wait();
 }
 
 using EncodeFn = PFN_cuTensorMapEncodeTiled_v12000;
@@ -362,7 +454,9 @@ static bool encode(CUtensorMap *m, const void *ptr, long long inner, long long r
 }
 
 template <class PL, int TILE, int STAGE>
-static cudaError_t launch_t(const ColTma &g, long long items, int ncols, cudaStream_t stream) {
+static cudaError_t launch_t(ColTma &g, long long items, int ncols, cudaStream_t stream) {
+  g.nat_swz = PL::L == 3072 ? 7 : 0;
+  if (const char *e = getenv("HK_COL_NATSWZ")) g.nat_swz = atoi(e) & 7;
   using LY = TmaLayout<PL, TILE, STAGE>;
   static std::atomic<unsigned long long> configured{0};
   static int sms[64] = {0};
@@ -408,6 +502,15 @@ static cudaError_t launch_cols_tma_t(int stage, const ColArgs &a, long long item
     if (!encode(&g.m_in, h.ptr, L2, g.rows_in, items, L2, h.item_stride, TILE) ||
         !encode(&g.m_in2, x.ptr, L2, g.rows_in2, items, L2, x.item_stride, TILE))
       return cudaErrorNotSupported;
+    // TMA stores of the Hermitian half (rows 0..L1/2 of both outputs)
+    const Out2 &o1 = a.out, &o2 = a.out2;
+    g.out_rows = o1.e1;
+    g.tma_out = getenv("HK_COLTMA_STORE") && o1.e1 == a.L1 / 2 + 1 && o2.e1 == o1.e1 &&
+                o1.e2 == L2 && o2.e2 == L2 && o1.len < 0 && o2.len < 0 &&
+                encode(&g.m_out, o1.ptr, 2 * L2, o1.e1, items, 2 * o1.s1, 2 * o1.item_stride,
+                       2 * TILE) &&
+                encode(&g.m_out2, o2.ptr, 2 * L2, o2.e1, items, 2 * o2.s1, 2 * o2.item_stride,
+                       2 * TILE);
     return launch_t<PL, TILE, ST_A_PAIR>(g, items, ncols, stream);
   }
   if (stage == ST_A_FWD || stage == ST_A_INV) {
@@ -420,6 +523,11 @@ static cudaError_t launch_cols_tma_t(int stage, const ColArgs &a, long long item
     const int f = cx ? 2 : 1;
     if (!encode(&g.m_in, op.ptr, f * L2, g.rows_in, items, f * L2, f * op.item_stride, f * TILE))
       return cudaErrorNotSupported;
+    const Out2 &o = a.out;
+    g.out_rows = std::min<int>(o.e1, a.L1);
+    g.tma_out = getenv("HK_COLTMA_STORE") &&
+                encode(&g.m_out, o.ptr, 2 * (long long)o.e2, g.out_rows, items, 2 * o.s1,
+                       2 * o.item_stride, 2 * TILE);
     return stage == ST_A_FWD ? launch_t<PL, TILE, ST_A_FWD>(g, items, ncols, stream)
                              : launch_t<PL, TILE, ST_A_INV>(g, items, ncols, stream);
   }
@@ -431,6 +539,13 @@ static cudaError_t launch_cols_tma_t(int stage, const ColArgs &a, long long item
     if (q.e1 < rows || !encode(&g.m_in, q.ptr, 2 * L2, rows, items, 2 * L2, 2 * q.item_stride,
                                2 * TILE))
       return cudaErrorNotSupported;
+    // y rows of L2 contiguous outputs: TMA stores when y is a whole number of rows
+    const Out2 &o = a.out;
+    g.out_rows = (int)std::min<long long>(o.len / L2, a.L1);
+    g.tma_out = getenv("HK_COLTMA_STORE") && o.len > 0 && o.len % L2 == 0 && o.s2 == 1 &&
+                o.s1 == L2 &&
+                encode(&g.m_out, o.ptr, 2 * L2, g.out_rows, items, 2 * L2, 2 * o.item_stride,
+                       2 * TILE);
     return launch_t<PL, TILE, ST_C>(g, items, ncols, stream);
   }
   return cudaErrorNotSupported;
