@@ -655,6 +655,36 @@ int tl_run(const hk_plan *p, const hk_operand &h, const hk_operand *xs, int nx, 
   }
   if ((int)fs.size() > p->order || (int)fs.size() > hk::kMaxFactors)
     return fail(HK_EUNSUPPORTED, "too many distinct vectors for the two-level workspace");
+  // 2-level block product with one distinct vector: the fused on-chip kernel
+  // (192 x 192 spectrum in four residue passes, hk_bhhb_fused.cu)
+  if (!p->twiddle && what == 0 && fs.size() == 1 && h.dtype == HK_C128 &&
+      fs[0].op.dtype == HK_C128 && fs[0].es == 1 && oes == 1 &&
+      p->inner[fs[0].mode] == p->inner[0] && p->outer[fs[0].mode] == p->outer[0]) {
+    const double2 *t48 = nullptr, *t192 = nullptr;  // cached per device by get_twiddles
+    int rc2 = get_twiddles(p->device, 48, &t48);
+    if (!rc2) rc2 = get_twiddles(p->device, 192, &t192);
+    if (!rc2) {
+      hk::bhhb::Args ba{};
+      ba.h = static_cast<const double2 *>(h.data);
+      ba.h_bstride = h.batch_stride;
+      ba.x = static_cast<const double2 *>(fs[0].op.data);
+      ba.x_bstride = fs[0].op.batch_stride;
+      ba.y = static_cast<double2 *>(out);
+      ba.y_bstride = out_stride;
+      ba.batch = batch;
+      ba.din = (int)p->dof[0];
+      ba.dout = (int)p->dof[1];
+      ba.n = (int)p->inner[0];
+      ba.N = (int)p->outer[0];
+      ba.power = fs[0].power;
+      ba.tw48 = t48;
+      ba.tw192 = t192;
+      ba.scale = 1.0 / (192.0 * 192.0);
+      const cudaError_t e = hk::launch_bhhb_fused(ba, st);
+      if (e == cudaSuccess) return HK_OK;
+      if (e != cudaErrorNotSupported) return cuda_fail(e, "fused block kernel launch");
+    }
+  }
   const long long chunk = tl_chunk(p, batch);
   double2 *W = static_cast<double2 *>(ws);
   double2 *Wh = W;

@@ -55,6 +55,23 @@ struct ColArgs {
 
 }  // namespace large
 
+namespace bhhb {
+// Fused BHHB product (hk_bhhb_fused.cu): one item per CTA, everything on chip.
+struct Args {
+  const double2 *h;  // (batch, din, dout) row-major: H[a][c] at a*dout + c
+  long long h_bstride;
+  const double2 *x;  // (batch, n*N) F-order: X[i][j] at i + n*j
+  long long x_bstride;
+  double2 *y;        // (batch, n*N) F-order
+  long long y_bstride;
+  long long batch;
+  int din, dout, n, N, power;
+  const double2 *tw48, *tw192;  // W_48^e, W_192^e
+  double scale;                 // 1 / 192^2
+};
+}  // namespace bhhb
+cudaError_t launch_bhhb_fused(const bhhb::Args &a, cudaStream_t stream);
+
 bool supported_col_len(long long L1);
 bool tma_col_len(long long L1);  // column lengths of the TMA column kernel
 cudaError_t launch_cols(int stage, const large::ColArgs &a, long long items, int ncols,
