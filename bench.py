@@ -616,7 +616,8 @@ def other_configs(torch, peak):
                         "(B_alg halves: 49,128 B/product); parity vs the reference's "
                         "complex128 outputs, north_star tolerance 1e-4"})
     del dh, dx, y64
-    # cfg3: one large real product (four-step, L = 1536 x 8192)
+    # cfg3: one large real product (four-step, L = 3072 x 4096: TMA column passes,
+    # ping-pong row stage)
     g = np.load(os.path.join(golden, "cfg3.npz"))
     h, x = workloads.cfg3()
     dh = torch.from_numpy(h).cuda()[None]
@@ -626,7 +627,7 @@ def other_configs(torch, peak):
     y = f3()[0].cpu().numpy()
     rec("cfg3", 1, ms, _relerr(y[g["idx"]], g["y"]))
     del dh, dx
-    # cfg4: 1024 BHHB products, 2D block kernels (L = 192 x 192)
+    # cfg4: 1024 BHHB products, 2D block kernels (192-point columns x 256-point rows)
     g = np.load(os.path.join(golden, "cfg4.npz"))
     Hb, X = workloads.cfg4()
     dH = torch.from_numpy(Hb).cuda()
