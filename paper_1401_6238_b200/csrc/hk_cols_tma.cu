@@ -256,7 +256,15 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
                                                                          s_store);
       __syncthreads();
     });
-    fast::pass<PL, PL::P - 1, INV, false, RL, RL, L1, true>(t, a.ctw, tw0, s_load, r_store);
+    // ST_C keeps only rows k < out_rows of y: when they fit in the first NOC
+    // outputs of every last-pass butterfly (k = k0 + j L1/RL, j < NOC), the
+    // pruned last pass computes NOC of the RL outputs
+    constexpr int NOC = 6;
+    const bool prune = SC && !g.tma_out && g.out_rows <= NOC * (L1 / RL);
+    if (prune)
+      fast::pass<PL, PL::P - 1, INV, false, RL, NOC, L1, true>(t, a.ctw, tw0, s_load, r_store);
+    else
+      fast::pass<PL, PL::P - 1, INV, false, RL, RL, L1, true>(t, a.ctw, tw0, s_load, r_store);
     __syncthreads();
     // digit-reversed registers -> natural order: register j of butterfly beta
     // holds frequency k = k(beta) + j * L1 / RL; single-operand stage A also
@@ -280,6 +288,7 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
       cplx cur = TW_A ? tw4(a, (long long)n2 * k0) : make_double2(1.0, 0.0);
 #pragma unroll
       for (int j = 0; j < RL; ++j) {
+        if (SC && prune && j >= NOC) break;
         cplx x = v[i * RL + j];
         if constexpr (TW_A) {
           x = INV ? cmulc(x, cur) : cmul(x, cur);

@@ -192,7 +192,7 @@ __device__ __forceinline__ void pass(int t, const C *__restrict__ tw, const TW0 
   // keeps the pass P-2 -> P-1 exchange inside each warp (see fft_dif).
   constexpr bool HIM = Tr::hi_major(p) && !HasChunk1<TW0>::value;
   constexpr int NIN = FINAL ? R : NZ;
-  constexpr int NOUT = FINAL ? NO : R;
+  constexpr int NOUT = NO;  // DIF passes: NO < R prunes outputs (callers pass R otherwise)
   // Pass-0 recurrence bases of a thread's NB butterflies, beta = t + i*T:
   // W_L^beta = W_L^t * W_L^{i T}, the second factor a compile-time constant,
   // so one table read serves all NB butterflies (8192 = 2 x 16^3: NB = 8).
@@ -310,7 +310,7 @@ __device__ __forceinline__ void pass(int t, const C *__restrict__ tw, const TW0 
         twiddle();
         DftP<R, false, R, NO>::run(a);
       } else {
-        DftP<R, INV, NZ, R>::run(a);
+        DftP<R, INV, NZ, NO>::run(a);
         twiddle();
       }
       pre_store();

@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
   constexpr int L = PL::L, T = PL::T, V = PL::V, R0 = PL::radix[0];
   constexpr int S0 = PL::stride(0);
   constexpr bool XD = NZ >= R0;
+  constexpr bool HD = (TWV & 64) != 0;  // h loaded directly (no TMA staging)
   constexpr int XS = XD ? 0 : NZ * S0;  // staged x elements
   constexpr int TW1 = L / R0;  // passes >= 1 read the compact W_{L/R0} table
   (void)Layout<PL>{};
@@ -260,6 +261,11 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
     return static_cast<const cplx *>(a.fac[0].ptr) +
            pp_off<XD>(a, blockIdx.x + k * gridDim.x, a.fac[0].bstride, a.fac[0].sstride);
   };
+  auto h_prefetch = [&](long long k) {  // HD: generator k of this CTA into L2
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(hptr(k)),
+                 "r"(((unsigned)a.h.len * 16u) & ~15u)
+                 : "memory");
+  };
   auto x_prefetch = [&](long long k) {  // XD: row k of this CTA into L2
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(xptr(k)),
                  "r"((unsigned)a.fac[0].len * 16u)
@@ -268,8 +274,13 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
   if (threadIdx.x == 0) {
     const uint32_t hbytes = (uint32_t)a.h.len * 16u, xbytes = (uint32_t)a.fac[0].len * 16u;
     if (nloc > 0) {
-      mbar_expect_tx(mb_h0, hbytes);
-      tma_load(smem_u32(hst), hptr(0), hbytes, mb_h0);
+      if constexpr (HD) {
+        h_prefetch(0);
+        if (nloc > 1) h_prefetch(1);
+      } else {
+        mbar_expect_tx(mb_h0, hbytes);
+        tma_load(smem_u32(hst), hptr(0), hbytes, mb_h0);
+      }
       if constexpr (XD) {
         x_prefetch(0);
       } else {
@@ -329,20 +340,35 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
       };
       cplx v[V];
       // ---- S = ifft(h~) from staged h; release hst to the TMA for product k+1
-      mbar_wait(mb_h0 + 8 * G, par);
       int t = fresh_t();
-      fast::fft_dif<PL, true, R0, TW1, REC>(
-          sbuf, t, a.tw1, tw0, [&](int pos) { return hst[pos]; },
-          v, sync, [&]() {
-            if (t == 0 && k + 1 < nloc) {
-              const uint32_t mb = mb_h0 + 8 * (1 - G);
-              const uint32_t bytes = (uint32_t)a.h.len * 16u;
-              fence_proxy_async();
-              mbar_expect_tx(mb, bytes);
-              tma_load(smem_u32(hst), hptr(k + 1), bytes, mb);
-            }
-          },
-          (WS *)nullptr, h_entry(kk));
+      if constexpr (HD) {
+        // h straight from global (hoisted loads, L2-prefetched a product ahead)
+        const cplx *hp = hptr(k);
+        const int hlen = a.h.len;
+        auto hl = [hp, hlen](int pos) {
+          return pos < hlen ? fast::ld_stream(hp + pos) : make_double2(0.0, 0.0);
+        };
+        fast::fft_dif<PL, true, R0, TW1, REC>(
+            sbuf, t, a.tw1, tw0, fast::Hoisted<decltype(hl)>{hl}, v, sync,
+            [&]() {
+              if (t == 0 && k + 2 < nloc) h_prefetch(k + 2);
+            },
+            (WS *)nullptr, h_entry(kk));
+      } else {
+        mbar_wait(mb_h0 + 8 * G, par);
+        fast::fft_dif<PL, true, R0, TW1, REC>(
+            sbuf, t, a.tw1, tw0, [&](int pos) { return hst[pos]; },
+            v, sync, [&]() {
+              if (t == 0 && k + 1 < nloc) {
+                const uint32_t mb = mb_h0 + 8 * (1 - G);
+                const uint32_t bytes = (uint32_t)a.h.len * 16u;
+                fence_proxy_async();
+                mbar_expect_tx(mb, bytes);
+                tma_load(smem_u32(hst), hptr(k + 1), bytes, mb);
+              }
+            },
+            (WS *)nullptr, h_entry(kk));
+      }
       if constexpr (SPLIT) war_arrive(mb_wx0 + 8 * G);
       tmem_wait_st();
 #pragma unroll
@@ -463,7 +489,7 @@ cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream) {
   // 24: TMEM pass-0 and pass-1 twiddles + split WAR barriers (r02: 169.4 us vs
   // 170.0 for 8 and 185.6 for 2 = recurrence for pass 1, the r01 default)
   int twv = 24;
-  if (const char *e = getenv("HK_PP_TWV")) twv = atoi(e) & 63;
+  if (const char *e = getenv("HK_PP_TWV")) twv = atoi(e) & 127;
   if (nz == 16 && !getenv("HK_NO_PP_ROWS")) {  // full rows (two-level row stage)
     const bool one = getenv("HK_PP_ROWS_TWO") == nullptr;  // A/B: two code copies
     if (no <= 4) return one ? pp::launch_pp<PL, 16, 4, 56>(a, stream) : pp::launch_pp<PL, 16, 4, 24>(a, stream);
@@ -474,6 +500,7 @@ cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream) {
       case 8: return pp::launch_pp<PL, 4, 4, 8>(a, stream);
       case 24: return pp::launch_pp<PL, 4, 4, 24>(a, stream);
       case 56: return pp::launch_pp<PL, 4, 4, 56>(a, stream);
+      case 88: return pp::launch_pp<PL, 4, 4, 88>(a, stream);
       case 6: return pp::launch_pp<PL, 4, 4, 6>(a, stream);
       case 1: return pp::launch_pp<PL, 4, 4, 1>(a, stream);
       case 2: return pp::launch_pp<PL, 4, 4, 2>(a, stream);
