@@ -582,7 +582,7 @@ namespace {
 int launch_row(long long L2, const Args1D &a, cudaStream_t st) {
   cudaError_t e = cudaErrorNotSupported;
   // 4096-point rows: the TMA ping-pong kernel (two row products per SM)
-  if (!g_force_generic && a.tw1) e = hk::launch_pp_1d((int)L2, a, st);
+  if (!g_force_generic) e = hk::launch_pp_1d((int)L2, a, st);
   if (!g_force_generic && e == cudaErrorNotSupported) e = hk::launch_fast_1d((int)L2, a, st);
   if (e == cudaErrorNotSupported) e = hk::launch_1d((int)L2, a, st);
   if (e != cudaSuccess) return cuda_fail(e, "row-stage kernel launch");

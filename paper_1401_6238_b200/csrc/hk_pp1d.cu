@@ -468,12 +468,230 @@ static cudaError_t launch_pp(const Args1D &a, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------
+// Batched short products (the 256-point row stage of the 2D block product,
+// cfg4): the ping-pong structure with "units" of GP = 256 / T products per
+// 256-thread group.  Each product's threads sit in one half-warp, so every
+// exchange of its three transforms is a warp sync; the group meets only where
+// the staging buffers change hands (after pass 0 of h and of x).
+//   smem: ex[2][GP * L] | hst[GP * L] (h rows of one unit, shared in turn) |
+//         xst[2][GP * XS] (x rows of this group's unit, XS = NZ * S0)
+//   TMEM: cols [0, 256) accumulators; [256, 320) the pass-0 twiddles W_L^{j t}
+//         (they depend on t = lane % T only: one slab for every warp)
+struct WarpEntry {
+  __device__ __forceinline__ void operator()() const { asm volatile("bar.warp.sync -1;\n" ::: "memory"); }
+};
+
+template <class PL, int NZ, int NO>
+__global__ void __launch_bounds__(512, 1) k_rows_pp(const __grid_constant__ Args1D a) {
+  constexpr int L = PL::L, T = PL::T, V = PL::V, R0 = PL::radix[0];
+  constexpr int GP = 256 / T;  // products per group
+  constexpr int S0 = PL::stride(0);
+  constexpr int XS = NZ * S0;
+  static_assert(PL::P == 2 && 32 % T == 0 && T * GP == 256, "two-pass plan, products within half-warps");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t mbar[4];  // full_h[0..1], full_x[0..1]
+  __shared__ uint32_t tmem_slot;
+  cplx *ex = reinterpret_cast<cplx *>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
+  cplx *hst = ex + 2 * GP * L;
+  cplx *xst = hst + GP * L;
+  const int warp = threadIdx.x >> 5;
+  const int g = threadIdx.x >> 8;
+  const int t_in = threadIdx.x & 255;
+  const int sub = t_in / T, t = t_in % T;
+  const uint32_t mb_h0 = smem_u32(&mbar[0]), mb_x0 = smem_u32(&mbar[2]);
+  // tails the TMA never writes: h rows past h.len, x rows past x.len
+  for (int i = threadIdx.x; i < GP * L; i += blockDim.x)
+    if (i % L >= a.h.len) hst[i] = make_double2(0.0, 0.0);
+  for (int i = threadIdx.x; i < 2 * GP * XS; i += blockDim.x)
+    if (i % XS >= a.fac[0].len) xst[i] = make_double2(0.0, 0.0);
+  fence_proxy_async();
+  if (warp == 0) tmem_alloc<512>(&tmem_slot);
+  if (threadIdx.x == 32) {
+    for (int i = 0; i < 4; ++i) mbar_init(smem_u32(&mbar[i]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t lane_q = (uint32_t)(32 * (warp & 3)) << 16;
+  const uint32_t tacc = tmem_slot + lane_q + (uint32_t)((warp >> 2) * 64);
+  const uint32_t ttw = tmem_slot + lane_q + 256u;
+  if (warp < 4) {  // one twiddle slab per lane quadrant serves all warps
+    const fast::Tw0Global g0{a.tw0, L / R0, R0};
+#pragma unroll
+    for (int c = 0; c < (R0 - 1 + 3) / 4; ++c) {
+      cplx w[4];
+      g0.chunk(t, c, w);
+      tmem_st4(ttw + 16 * c, w);
+    }
+    tmem_wait_st();
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const Tw0Tmem tw0{ttw};
+
+  const long long nunits = (a.batch + GP - 1) / GP;
+  const long long nloc = nunits > blockIdx.x ? (nunits - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto row_off = [&](long long b, long long bs, long long ss) {
+    const long long ob = b / a.nsub;
+    return ob * bs + (b - ob * a.nsub) * ss;
+  };
+  struct Unit {
+    long long b0;
+    int nr;
+  };
+  auto unit_rows = [&](long long k) {  // first row and row count of unit k
+    const long long b0 = (blockIdx.x + k * gridDim.x) * GP;
+    return Unit{b0, (int)(a.batch - b0 < GP ? a.batch - b0 : GP)};
+  };
+  auto issue_h = [&](long long k, uint32_t mb) {
+    const Unit u = unit_rows(k);
+    const long long b0 = u.b0;
+    const int nr = u.nr;
+    const uint32_t bytes = (uint32_t)a.h.len * 16u;
+    mbar_expect_tx(mb, bytes * nr);
+    for (int r = 0; r < nr; ++r)
+      tma_load(smem_u32(hst + r * L),
+               static_cast<const cplx *>(a.h.ptr) + row_off(b0 + r, a.h.bstride, a.h.sstride), bytes, mb);
+  };
+  auto issue_x = [&](long long k, cplx *dst, uint32_t mb) {
+    const Unit u = unit_rows(k);
+    const long long b0 = u.b0;
+    const int nr = u.nr;
+    const uint32_t bytes = (uint32_t)a.fac[0].len * 16u;
+    mbar_expect_tx(mb, bytes * nr);
+    for (int r = 0; r < nr; ++r)
+      tma_load(smem_u32(dst + r * XS),
+               static_cast<const cplx *>(a.fac[0].ptr) +
+                   row_off(b0 + r, a.fac[0].bstride, a.fac[0].sstride),
+               bytes, mb);
+  };
+  if (threadIdx.x == 0) {
+    if (nloc > 0) {
+      issue_h(0, mb_h0);
+      issue_x(0, xst, mb_x0);
+    }
+    if (nloc > 1) issue_x(1, xst + GP * XS, mb_x0 + 8);
+  }
+
+  const fast::WarpSync wsync;
+  // staging hand-off at a group barrier after pass 0 (measured against
+  // last-warp counters with fully warp-decoupled products: 922 vs 952 us, cfg4)
+  const GroupBar<256> gsync{1 + g};
+  cplx *sbuf = ex + g * GP * L + sub * L;
+  cplx *my_x = xst + g * GP * XS;
+  int kk = 0;
+  for (long long k = g; k < nloc; k += 2, ++kk) {
+    const uint32_t par = (uint32_t)(kk & 1);
+    const Unit un = unit_rows(k);
+    const long long b0 = un.b0;
+    const bool active = sub < un.nr;
+    cplx v[V];
+    // ---- S = ifft(h~) of this thread's row; hst goes to the TMA for unit k+1
+    mbar_wait(mb_h0 + 8 * g, par);
+    fast::fft_dif<PL, true, R0>(
+        sbuf, t, a.tw, tw0, [&](int pos) { return hst[sub * L + pos]; }, v, gsync,
+        [&]() {
+          if (k + 1 < nloc && t_in == 0) {
+            fence_proxy_async();
+            issue_h(k + 1, mb_h0 + 8 * (1 - g));
+          }
+        },
+        (void *)nullptr, WarpEntry{});
+    tmem_wait_st();
+#pragma unroll
+    for (int c = 0; c < V / 4; ++c) tmem_st4(tacc + 16 * c, &v[4 * c]);
+    // ---- X = fft(x~); this group's xst is refilled with unit k+2
+    mbar_wait(mb_x0 + 8 * g, par);
+    fast::fft_dif<PL, false, NZ>(
+        sbuf, t, a.tw, tw0, [&](int pos) { return my_x[sub * XS + pos]; }, v, gsync,
+        [&]() {
+          if (k + 2 < nloc && t_in == 0) {
+            fence_proxy_async();
+            issue_x(k + 2, my_x, mb_x0 + 8 * g);
+          }
+        },
+        (void *)nullptr, WarpEntry{});
+    tmem_wait_st();
+#pragma unroll
+    for (int c = 0; c < V / 4; ++c) {
+      cplx acc[4];
+      tmem_ld4(tacc + 16 * c, acc);
+      for (int q = 0; q < a.fac[0].power; ++q) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[e] = cmul(acc[e], v[4 * c + e]);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[4 * c + e] = acc[e];
+    }
+    // ---- y = fft(acc)[:n_1] (warp-local exchanges only)
+    cplx *yk = static_cast<cplx *>(a.out) + row_off(b0 + sub, a.out_bstride, a.out_sstride);
+    fast::fft_final<PL, NO>(
+        sbuf, t, a.tw, tw0, v,
+        [&](int pos, cplx val) {
+          if (active && pos < a.out_len) yk[pos] = make_double2(val.x * a.scale, val.y * a.scale);
+        },
+        wsync);
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tmem_fence_after();
+    tmem_dealloc<512>(tmem_slot);
+  }
+}
+
+template <class PL, int NZ, int NO>
+static cudaError_t launch_rows_pp(const Args1D &a, cudaStream_t stream) {
+  constexpr int GP = 256 / PL::T;
+  constexpr int XS = NZ * PL::stride(0);
+  const int smem = (3 * GP * PL::L + 2 * GP * XS) * (int)sizeof(cplx) + 128;
+  static std::atomic<unsigned long long> configured{0};
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(configured.load() & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(k_rows_pp<PL, NZ, NO>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+    configured.fetch_or(bit);
+  }
+  const long long units = (a.batch + GP - 1) / GP;
+  long long grid = std::min<long long>(units, sms[dev & 63]);
+  if (grid <= 0) return cudaSuccess;
+  k_rows_pp<PL, NZ, NO><<<(unsigned)grid, 512, smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
 }  // namespace pp
 
 // Ping-pong TMA path; cudaErrorNotSupported unless the request is the plain
 // batched H x^{m-1} shape it implements.
+// 256-point batched rows (2D block row stage) on the ping-pong kernel.
+static cudaError_t launch_pp_256(const Args1D &a, cudaStream_t stream) {
+  if (getenv("HK_NO_PP256")) return cudaErrorNotSupported;
+  if (a.mode != M_PARTIAL || a.nfac != 1 || !a.tw0 || a.nsub < 1 || a.ncombo)
+    return cudaErrorNotSupported;
+  const Factor &h = a.h, &x = a.fac[0];
+  if (h.kind != FK_C128 || x.kind != FK_C128 || h.estride != 1 || x.estride != 1 ||
+      a.out_estride != 1 || h.len > 256 || h.len <= 0 || x.len <= 0 || x.len > 64)
+    return cudaErrorNotSupported;
+  if ((reinterpret_cast<uintptr_t>(h.ptr) | reinterpret_cast<uintptr_t>(x.ptr)) & 15)
+    return cudaErrorNotSupported;
+  using PL = Plan1D<256, 16, 16, 16>;
+  const int no = (a.out_len + 15) / 16;
+  if (no <= 4) return pp::launch_rows_pp<PL, 4, 4>(a, stream);
+  return pp::launch_rows_pp<PL, 4, 16>(a, stream);
+}
+
 cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream) {
   if (getenv("HK_NO_PP")) return cudaErrorNotSupported;
+  if (L == 256) return launch_pp_256(a, stream);
   if (L != 4096 || a.mode != M_PARTIAL || a.nfac != 1 || !a.tw0 || a.nsub < 1 || a.ncombo)
     return cudaErrorNotSupported;
   const Factor &h = a.h, &x = a.fac[0];
