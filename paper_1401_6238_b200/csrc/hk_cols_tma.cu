@@ -97,6 +97,25 @@ __device__ __forceinline__ cplx tw4(const ColArgs &a, long long e) {
   return cmul(__ldg(&a.thi[e >> 12]), __ldg(&a.tlo[e & 4095]));
 }
 
+// Column-pass twiddles in TMEM (r02): a thread's twiddles are the same for
+// every tile (pass 0: W_L1^{j beta} of its NB0 butterflies, pass 1: W_256^{j lo}),
+// so they are read once from the W_L1 table and kept next to nothing else in
+// TMEM -- no dependent table reads and no recurrence per tile.
+template <class PL>
+struct ColTw {
+  static constexpr int R0 = PL::radix[0], R1 = PL::radix[1], T = PL::T;
+  static constexpr int NB0 = (PL::L / R0 + T - 1) / T;  // pass-0 butterflies per thread
+  static constexpr int NC0 = (R0 - 1 + 3) / 4, NC1 = (R1 - 1 + 3) / 4;
+  static constexpr int SLAB = (NB0 * NC0 + NC1) * 16;  // columns per warp slab
+  uint32_t taddr;
+  __device__ __forceinline__ void chunk(int beta, int c, cplx *w) const {
+    tmem_ld4(taddr + 16 * ((beta / T) * NC0 + c), w);
+  }
+  __device__ __forceinline__ void chunk1(int c, cplx *w) const {
+    tmem_ld4(taddr + 16 * (NB0 * NC0 + c), w);
+  }
+};
+
 template <class PL, int TILE, int STAGE>
 struct TmaLayout {
   static constexpr int L1 = PL::L;
@@ -164,7 +183,49 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
   __syncthreads();
   long long w = blockIdx.x;
   if (threadIdx.x == 0 && w < ntiles) issue(w);
-  const fast::Tw0Rec tw0{a.ctw};
+  // ---- twiddle slabs in TMEM (see ColTw); 12 warps: three slabs per lane quadrant
+  using CT = ColTw<PL>;
+  static_assert(((TILE * T / 32 + 3) / 4) * CT::SLAB <= 512, "twiddle slabs exceed TMEM");
+  static_assert(PL::P == 3, "pass-1 twiddle slab assumes a three-pass column plan");
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc<512>(&tmem_slot);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const CT tw0{tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * CT::SLAB)};
+  {
+    const int tp = threadIdx.x / TILE, tc = threadIdx.x % T;
+#pragma unroll
+    for (int i = 0; i < CT::NB0; ++i) {
+      const int beta = tp + i * T;
+#pragma unroll
+      for (int c = 0; c < CT::NC0; ++c) {
+        cplx w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = 4 * c + q + 1;
+          w[q] = (j < R0 && beta < L1 / R0) ? __ldg(&a.ctw[(j * beta) % L1])
+                                             : make_double2(1.0, 0.0);
+        }
+        tmem_st4(tw0.taddr + 16 * (i * CT::NC0 + c), w);
+      }
+    }
+    // pass 1 (lo-major with a per-thread slab, fast::pass): lo = t mod stride(1)
+    constexpr int S1 = PL::stride(1), RR1 = PL::radix[1], LP1 = S1 * RR1;
+    const int lo = tc % S1;
+#pragma unroll
+    for (int c = 0; c < CT::NC1; ++c) {
+      cplx w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = 4 * c + q + 1;
+        w[q] = j < RR1 ? __ldg(&a.ctw[(j * lo * (L1 / LP1)) % L1]) : make_double2(1.0, 0.0);
+      }
+      tmem_st4(tw0.taddr + 16 * (CT::NB0 * CT::NC0 + c), w);
+    }
+    tmem_wait_st();
+  }
 
   for (int it = 0; w < ntiles; ++it, w += gridDim.x) {
     const long long item = w / tiles_per_item;
@@ -428,6 +489,12 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
     __syncthreads();  // exchange buffer reused by the next tile's pass 0
   }
   if (g.tma_out && threadIdx.x == 0) tma::bulk_wait();
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tmem_fence_after();
+    tmem_dealloc<512>(tmem_slot);
+  }
 }
 
 using EncodeFn = PFN_cuTensorMapEncodeTiled_v12000;
