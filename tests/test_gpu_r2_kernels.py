@@ -113,3 +113,28 @@ def test_cfg2_kernel_variants(monkeypatch, twv):
     np.testing.assert_allclose(np.linalg.norm(y, axis=1), g["norms"][:B], rtol=TOL)
     ref = O.hankel_tvp_partial(h[0], (1024,) * 4, [x[0]] * 3)
     assert strict_relerr(y[0], ref) <= TOL
+
+
+@pytest.mark.parametrize("block,outer,B", [((64, 64, 64), (20, 20, 20), 3),   # 64-point columns
+                                           ((60, 60, 60), (64, 64, 64), 2),
+                                           ((64, 64), (50, 50), 5),
+                                           ((32, 32, 32), (40, 40, 40), 3)])  # 96-point rows
+def test_block_rows_pp256_vs_fast_rows(monkeypatch, block, outer, B):
+    """The 256-point row kernel (units of 16 rows, several items per launch)
+    against the fast-kernel row stage and the oracle."""
+    rng = np.random.default_rng(sum(block) * 3 + sum(outer) + B)
+    m = len(block)
+    din, dout = sum(block) - m + 1, sum(outer) - m + 1
+    H = rand_vec(rng, B * din * dout).reshape(B, din, dout)
+    X = rand_vec(rng, B * block[1] * outer[1]).reshape(B, outer[1], block[1])  # (B, N, n)
+    dH = torch.from_numpy(H).cuda()
+    dx = torch.from_numpy(np.ascontiguousarray(X)).cuda().reshape(B, -1)
+    xs = [dx] * (m - 1)
+    y = batched.bhhb_tvp_partial(dH, xs, m, block, outer).cpu().numpy()
+    monkeypatch.setenv("HK_NO_PP256", "1")
+    y2 = batched.bhhb_tvp_partial(dH, xs, m, block, outer).cpu().numpy()
+    assert strict_relerr(y, y2) <= 1e-13
+    for b in range(B):
+        xv = X[b].reshape(-1)
+        ref = O.bhhb_tvp_partial(H[b], block, outer, [xv] * (m - 1))
+        assert strict_relerr(y[b], ref) <= TOL
