@@ -19,11 +19,17 @@ from . import _native as N
 from . import batched
 
 
+_CUDA_OK = False
+
+
 def require_cuda() -> int:
-    if not torch.cuda.is_available():
-        raise RuntimeError(
-            "no CUDA device: the hankelfft_b200 product path runs only on the GPU "
-            "(there is no CPU fallback)")
+    global _CUDA_OK
+    if not _CUDA_OK:
+        if not torch.cuda.is_available():
+            raise RuntimeError(
+                "no CUDA device: the hankelfft_b200 product path runs only on the GPU "
+                "(there is no CPU fallback)")
+        _CUDA_OK = True
     return torch.cuda.current_device()
 
 
@@ -126,6 +132,7 @@ class HankelDeviceCache:
         self.shape = tuple(shape)
         self.h = h
         self._per_dev = {}
+        self._lean = {}  # dev -> (plan, operand struct of the latency path or None)
 
     def _state(self) -> tuple:
         dev = require_cuda()
@@ -149,24 +156,32 @@ class HankelDeviceCache:
     def tvp_partial(self, xs) -> np.ndarray:
         dev, (dh, spec) = self._state()
         uniq, idx = _dedupe(xs)
-        plan = batched.hankel_plan(self.shape, dev)
-        if plan.workspace_per_item == 0:
-            if plan.fft_lens[0] <= self.SMALL_L:
-                return self._lean_partial(dev, dh, uniq, idx, N.HK_C128)
-            return self._lean_partial(dev, spec, uniq, idx)
+        lean = self._lean.get(dev)
+        if lean is None:
+            plan = batched.hankel_plan(self.shape, dev)
+            if plan.workspace_per_item == 0:
+                small = plan.fft_lens[0] <= self.SMALL_L
+                src = dh if small else spec
+                # the operand struct and plan handle of the latency path, built once
+                hop = N.Operand(src.data_ptr(), src.stride(0),
+                                N.HK_C128 if small else N.HK_SPEC, 0)
+                lean = self._lean[dev] = (plan, hop)
+            else:
+                lean = self._lean[dev] = (plan, None)
+        plan, hop = lean
+        if hop is not None:
+            st = _Staging.get(dev)
+            with st.lock:
+                return self._lean_locked(st, dev, plan, hop, uniq, idx)
         with _Staging.get(dev).lock:
             up = _upload_packed(uniq, dev)
             y = batched.hankel_tvp_partial(spec, [up[i] for i in idx], self.shape, spectrum=True)
             return _download(y[0])
 
-    def _lean_partial(self, dev, spec, uniq, idx, hkind=N.HK_SPEC) -> np.ndarray:
-        """Latency path: one packed pinned H2D copy, a direct C-ABI call with
-        cached plan/operand structs, one pinned D2H copy, one stream sync."""
-        st = _Staging.get(dev)
-        with st.lock:
-            return self._lean_locked(st, dev, spec, uniq, idx, hkind)
-
-    def _lean_locked(self, st, dev, spec, uniq, idx, hkind) -> np.ndarray:
+    def _lean_locked(self, st, dev, plan, hop, uniq, idx) -> np.ndarray:
+        """Latency path: the vectors packed into one pinned buffer, one C-ABI
+        call (zero-copy product or H2D + product + D2H) and one stream sync,
+        with the plan and operand structs cached per device."""
         n_in = sum(a.shape[0] for a in uniq)
         n1 = self.shape[0]
         st.ensure(n_in + n1)
@@ -177,11 +192,8 @@ class HankelDeviceCache:
             offs.append(off)
             off += a.shape[0]
         stream = torch.cuda.current_stream(dev)
-        plan = batched.hankel_plan(self.shape, dev)
         xoff = (ctypes.c_int64 * len(idx))(*[offs[i] for i in idx])
-        hop = N.Operand(spec.data_ptr(), spec.stride(0), hkind, 0)
         dbase, hbase = st.dbase, st.hbase
-        # one C call: H2D of the packed vectors, the product, D2H of y, sync
         N.check(N.load_library().hk_tvp_partial_host(
             plan.handle, hop, hbase, n_in, xoff, len(idx), dbase, dbase + 16 * n_in,
             hbase + 16 * n_in, ctypes.c_void_p(stream.cuda_stream)), "hk_tvp_partial_host")

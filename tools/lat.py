@@ -21,3 +21,17 @@ print("_dedupe             %.1f us" % t(lambda: D._dedupe(vecs)))
 print("hankel_plan         %.1f us" % t(lambda: batched.hankel_plan((100,) * 3, 0)))
 print("current_stream      %.1f us" % t(lambda: torch.cuda.current_stream(0)))
 print("cuda sync (idle)    %.1f us" % t(lambda: torch.cuda.synchronize()))
+# raw C-ABI latency call (pinned zero-copy, kernel, stream sync) with prebuilt arguments
+st = D._Staging.get(0)
+plan, hop = H._dev._lean[0]
+uniq, idx = D._dedupe(vecs)
+n_in = sum(a.shape[0] for a in uniq)
+st.ensure(n_in + 100)
+xoff = (ctypes.c_int64 * len(idx))(*[0 for i in idx])
+lib = N.load_library()
+sp = ctypes.c_void_p(torch.cuda.current_stream(0).cuda_stream)
+fn = lambda: lib.hk_tvp_partial_host(plan.handle, hop, st.hbase, n_in, xoff, len(idx), st.dbase,
+                                     st.dbase + 16 * n_in, st.hbase + 16 * n_in, sp)
+print("raw C call          %.1f us" % t(fn))
+print("require_cuda        %.1f us" % t(lambda: D.require_cuda()))
+print("_state              %.1f us" % t(lambda: H._dev._state()))
