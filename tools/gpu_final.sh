@@ -15,6 +15,7 @@ cap cfg2_pp k_hankel_pp 2 "cfg2 2"
 cap cfg3_colA k_cols_tma 2 "cfg3 1"
 cap cfg3_rows k_hankel_pp 1 "cfg3 1"
 cap cfg3_colC k_cols_tma 3 "cfg3 1"
-cap cfg4_rows k_hankel_fast 1 "cfg4 1"
+cap cfg4_rows k_rows_pp 1 "cfg4 1"
+cap cfg4_xcols k_cols 1 "cfg4 1"
 cap cfg5_combo k_hankel_fast 4 "cfg5 1"
 echo done > gpurun_out/f_done
