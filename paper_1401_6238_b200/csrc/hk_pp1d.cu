@@ -483,33 +483,39 @@ struct WarpEntry {
   __device__ __forceinline__ void operator()() const { asm volatile("bar.warp.sync -1;\n" ::: "memory"); }
 };
 
-template <class PL, int NZ, int NO>
+// NG groups of 512/NG threads; NH h staging buffers (unit k uses hst[k % NH]
+// and, once consumed, is refilled with unit k + NH for group (g + NH) % NG).
+template <class PL, int NZ, int NO, int NG, int NH>
 __global__ void __launch_bounds__(512, 1) k_rows_pp(const __grid_constant__ Args1D a) {
   constexpr int L = PL::L, T = PL::T, V = PL::V, R0 = PL::radix[0];
-  constexpr int GP = 256 / T;  // products per group
+  constexpr int GT = 512 / NG;  // threads per group
+  constexpr int GP = GT / T;    // products per group (one unit)
   constexpr int S0 = PL::stride(0);
   constexpr int XS = NZ * S0;
-  static_assert(PL::P == 2 && 32 % T == 0 && T * GP == 256, "two-pass plan, products within half-warps");
+  static_assert(PL::P == 2 && 32 % T == 0 && T * GP == GT && NG % NH == 0,
+                "two-pass plan, products within half-warps");
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t mbar[4];  // full_h[0..1], full_x[0..1]
+  // full_h[NG], full_x[NG]: one barrier per GROUP (not per buffer), so a
+  // waiter can never see a phase two completions old on a shared barrier
+  __shared__ __align__(8) uint64_t mbar[2 * NG];
   __shared__ uint32_t tmem_slot;
   cplx *ex = reinterpret_cast<cplx *>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
-  cplx *hst = ex + 2 * GP * L;
-  cplx *xst = hst + GP * L;
+  cplx *hst = ex + NG * GP * L;
+  cplx *xst = hst + NH * GP * L;
   const int warp = threadIdx.x >> 5;
-  const int g = threadIdx.x >> 8;
-  const int t_in = threadIdx.x & 255;
+  const int g = threadIdx.x / GT;
+  const int t_in = threadIdx.x % GT;
   const int sub = t_in / T, t = t_in % T;
-  const uint32_t mb_h0 = smem_u32(&mbar[0]), mb_x0 = smem_u32(&mbar[2]);
+  const uint32_t mb_h0 = smem_u32(&mbar[0]), mb_x0 = smem_u32(&mbar[NG]);
   // tails the TMA never writes: h rows past h.len, x rows past x.len
-  for (int i = threadIdx.x; i < GP * L; i += blockDim.x)
+  for (int i = threadIdx.x; i < NH * GP * L; i += blockDim.x)
     if (i % L >= a.h.len) hst[i] = make_double2(0.0, 0.0);
-  for (int i = threadIdx.x; i < 2 * GP * XS; i += blockDim.x)
+  for (int i = threadIdx.x; i < NG * GP * XS; i += blockDim.x)
     if (i % XS >= a.fac[0].len) xst[i] = make_double2(0.0, 0.0);
   fence_proxy_async();
   if (warp == 0) tmem_alloc<512>(&tmem_slot);
   if (threadIdx.x == 32) {
-    for (int i = 0; i < 4; ++i) mbar_init(smem_u32(&mbar[i]), 1);
+    for (int i = 0; i < 2 * NG; ++i) mbar_init(smem_u32(&mbar[i]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   tmem_fence_before();
@@ -547,14 +553,16 @@ __global__ void __launch_bounds__(512, 1) k_rows_pp(const __grid_constant__ Args
     const long long b0 = (blockIdx.x + k * gridDim.x) * GP;
     return Unit{b0, (int)(a.batch - b0 < GP ? a.batch - b0 : GP)};
   };
-  auto issue_h = [&](long long k, uint32_t mb) {
+  auto issue_h = [&](long long k) {  // unit k into hst[k % NH]
     const Unit u = unit_rows(k);
     const long long b0 = u.b0;
     const int nr = u.nr;
     const uint32_t bytes = (uint32_t)a.h.len * 16u;
+    const uint32_t mb = mb_h0 + 8 * (uint32_t)(k % NG);  // the group of unit k
+    cplx *dst = hst + (k % NH) * GP * L;
     mbar_expect_tx(mb, bytes * nr);
     for (int r = 0; r < nr; ++r)
-      tma_load(smem_u32(hst + r * L),
+      tma_load(smem_u32(dst + r * L),
                static_cast<const cplx *>(a.h.ptr) + row_off(b0 + r, a.h.bstride, a.h.sstride), bytes, mb);
   };
   auto issue_x = [&](long long k, cplx *dst, uint32_t mb) {
@@ -570,34 +578,35 @@ __global__ void __launch_bounds__(512, 1) k_rows_pp(const __grid_constant__ Args
                bytes, mb);
   };
   if (threadIdx.x == 0) {
-    if (nloc > 0) {
-      issue_h(0, mb_h0);
-      issue_x(0, xst, mb_x0);
-    }
-    if (nloc > 1) issue_x(1, xst + GP * XS, mb_x0 + 8);
+    for (int k = 0; k < NH && k < nloc; ++k) issue_h(k);
+    for (int k = 0; k < NG && k < nloc; ++k) issue_x(k, xst + k * GP * XS, mb_x0 + 8 * k);
   }
 
   const fast::WarpSync wsync;
   // staging hand-off at a group barrier after pass 0 (measured against
   // last-warp counters with fully warp-decoupled products: 922 vs 952 us, cfg4)
-  const GroupBar<256> gsync{1 + g};
+  // one-warp groups hand off at a warp sync (named barriers run out at 16)
+  using GSync = std::conditional_t<GT == 32, fast::WarpSync, GroupBar<GT>>;
+  GSync gsync;
+  if constexpr (GT != 32) gsync = GSync{1 + g};
   cplx *sbuf = ex + g * GP * L + sub * L;
   cplx *my_x = xst + g * GP * XS;
   int kk = 0;
-  for (long long k = g; k < nloc; k += 2, ++kk) {
-    const uint32_t par = (uint32_t)(kk & 1);
+  for (long long k = g; k < nloc; k += NG, ++kk) {
+    const uint32_t par = (uint32_t)(kk & 1);  // this group's kk-th unit
     const Unit un = unit_rows(k);
     const long long b0 = un.b0;
     const bool active = sub < un.nr;
     cplx v[V];
     // ---- S = ifft(h~) of this thread's row; hst goes to the TMA for unit k+1
+    const cplx *hk = hst + (k % NH) * GP * L;
     mbar_wait(mb_h0 + 8 * g, par);
     fast::fft_dif<PL, true, R0>(
-        sbuf, t, a.tw, tw0, [&](int pos) { return hst[sub * L + pos]; }, v, gsync,
+        sbuf, t, a.tw, tw0, [&](int pos) { return hk[sub * L + pos]; }, v, gsync,
         [&]() {
-          if (k + 1 < nloc && t_in == 0) {
+          if (k + NH < nloc && t_in == 0) {
             fence_proxy_async();
-            issue_h(k + 1, mb_h0 + 8 * (1 - g));
+            issue_h(k + NH);
           }
         },
         (void *)nullptr, WarpEntry{});
@@ -609,9 +618,9 @@ __global__ void __launch_bounds__(512, 1) k_rows_pp(const __grid_constant__ Args
     fast::fft_dif<PL, false, NZ>(
         sbuf, t, a.tw, tw0, [&](int pos) { return my_x[sub * XS + pos]; }, v, gsync,
         [&]() {
-          if (k + 2 < nloc && t_in == 0) {
+          if (k + NG < nloc && t_in == 0) {
             fence_proxy_async();
-            issue_x(k + 2, my_x, mb_x0 + 8 * g);
+            issue_x(k + NG, my_x, mb_x0 + 8 * g);
           }
         },
         (void *)nullptr, WarpEntry{});
@@ -644,18 +653,18 @@ __global__ void __launch_bounds__(512, 1) k_rows_pp(const __grid_constant__ Args
   }
 }
 
-template <class PL, int NZ, int NO>
+template <class PL, int NZ, int NO, int NG, int NH>
 static cudaError_t launch_rows_pp(const Args1D &a, cudaStream_t stream) {
-  constexpr int GP = 256 / PL::T;
+  constexpr int GP = 512 / NG / PL::T;
   constexpr int XS = NZ * PL::stride(0);
-  const int smem = (3 * GP * PL::L + 2 * GP * XS) * (int)sizeof(cplx) + 128;
+  const int smem = ((NG + NH) * GP * PL::L + NG * GP * XS) * (int)sizeof(cplx) + 128;
   static std::atomic<unsigned long long> configured{0};
   static int sms[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(configured.load() & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(k_rows_pp<PL, NZ, NO>,
+    cudaError_t e = cudaFuncSetAttribute(k_rows_pp<PL, NZ, NO, NG, NH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
@@ -664,14 +673,12 @@ static cudaError_t launch_rows_pp(const Args1D &a, cudaStream_t stream) {
   const long long units = (a.batch + GP - 1) / GP;
   long long grid = std::min<long long>(units, sms[dev & 63]);
   if (grid <= 0) return cudaSuccess;
-  k_rows_pp<PL, NZ, NO><<<(unsigned)grid, 512, smem, stream>>>(a);
+  k_rows_pp<PL, NZ, NO, NG, NH><<<(unsigned)grid, 512, smem, stream>>>(a);
   return cudaGetLastError();
 }
 
 }  // namespace pp
 
-// Ping-pong TMA path; cudaErrorNotSupported unless the request is the plain
-// batched H x^{m-1} shape it implements.
 // 256-point batched rows (2D block row stage) on the ping-pong kernel.
 static cudaError_t launch_pp_256(const Args1D &a, cudaStream_t stream) {
   if (getenv("HK_NO_PP256")) return cudaErrorNotSupported;
@@ -685,10 +692,21 @@ static cudaError_t launch_pp_256(const Args1D &a, cudaStream_t stream) {
     return cudaErrorNotSupported;
   using PL = Plan1D<256, 16, 16, 16>;
   const int no = (a.out_len + 15) / 16;
-  if (no <= 4) return pp::launch_rows_pp<PL, 4, 4>(a, stream);
-  return pp::launch_rows_pp<PL, 4, 16>(a, stream);
+  // Groups of the row kernel (B200 cfg4, us): 2 x 256 threads / 1 h buffer
+  // 918, 4 x 128 / 2 buffers 890, 8 x 64 / 4 buffers 840, 16 one-warp groups /
+  // 8 buffers 784 (default; HK_ROWS_NG selects the others for A/B)
+  const int ng = getenv("HK_ROWS_NG") ? atoi(getenv("HK_ROWS_NG")) : 16;
+  if (no <= 4) {
+    if (ng == 2) return pp::launch_rows_pp<PL, 4, 4, 2, 1>(a, stream);
+    if (ng == 4) return pp::launch_rows_pp<PL, 4, 4, 4, 2>(a, stream);
+    if (ng == 8) return pp::launch_rows_pp<PL, 4, 4, 8, 4>(a, stream);
+    return pp::launch_rows_pp<PL, 4, 4, 16, 8>(a, stream);
+  }
+  return pp::launch_rows_pp<PL, 4, 16, 16, 8>(a, stream);
 }
 
+// Ping-pong TMA path; cudaErrorNotSupported unless the request is the plain
+// batched H x^{m-1} shape it implements.
 cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream) {
   if (getenv("HK_NO_PP")) return cudaErrorNotSupported;
   if (L == 256) return launch_pp_256(a, stream);
