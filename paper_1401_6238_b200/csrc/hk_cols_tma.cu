@@ -90,6 +90,15 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 __device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
+// named barrier with a runtime id over N threads (one column group)
+template <int N>
+struct GroupBar {
+  int id;
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "n"(N) : "memory");
+  }
+};
+
 }  // namespace tma
 
 __device__ __forceinline__ cplx tw4(const ColArgs &a, long long e) {
@@ -135,7 +144,10 @@ struct TmaLayout {
   static_assert(L1 % BR == 0, "column length must be a multiple of the box height");
 };
 
-template <class PL, int TILE, int STAGE>
+// DEC: the TILE columns run as independent thread groups (named barriers per
+// column); they meet only when the landing buffer is refilled, which the
+// last group to finish its pass 0 triggers.  Otherwise CTA-wide barriers.
+template <class PL, int TILE, int STAGE, bool DEC>
 __global__ void __launch_bounds__(TILE * PL::T, 1)
     k_cols_tma(const __grid_constant__ ColTma g, int tiles_per_item, long long ntiles) {
   using LY = TmaLayout<PL, TILE, STAGE>;
@@ -155,6 +167,15 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
   cplx *ex = reinterpret_cast<cplx *>(base + LY::LAND);
   const uint32_t mb = smem_u32(&mbar);
   const int lrows = (SC && a.half) ? ((L1 / 2 + 1 + BR - 1) / BR) * BR : L1;
+  __shared__ int land_rel;  // DEC: column groups done with the landing buffer
+  const int cg = threadIdx.x / T;  // DEC: this thread's column group
+  const tma::GroupBar<T> gbar_{1 + cg};
+  auto bar = [&]() {
+    if constexpr (DEC)
+      gbar_();
+    else
+      __syncthreads();
+  };
 
   auto issue = [&](long long w) {
     const long long item = w / tiles_per_item;
@@ -178,6 +199,7 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
 
   if (threadIdx.x == 0) {
     tma::mbar_init(mb, 1);
+    land_rel = 0;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -195,7 +217,8 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
   tmem_fence_after();
   const CT tw0{tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * CT::SLAB)};
   {
-    const int tp = threadIdx.x / TILE, tc = threadIdx.x % T;
+    const int tc = threadIdx.x % T;
+    const int tp = DEC ? tc : threadIdx.x / TILE;  // pass-0 thread index
 #pragma unroll
     for (int i = 0; i < CT::NB0; ++i) {
       const int beta = tp + i * T;
@@ -236,10 +259,13 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
       if constexpr (SC) __syncthreads();
     }
     if constexpr (!SC) {
-      // partial last rows of the operands (the maps cover full rows only)
-      if (threadIdx.x < 2 * TILE) {
-        const int c = threadIdx.x % TILE;
-        const bool second = threadIdx.x >= TILE;
+      // partial last rows of the operands (the maps cover full rows only);
+      // DEC: threads 0 and 1 of each column group patch that column
+      const int tf = DEC ? (threadIdx.x % T) * TILE + cg : (int)threadIdx.x;
+      const bool fixer = DEC ? (threadIdx.x % T) < 2 : threadIdx.x < 2 * TILE;
+      if (fixer) {
+        const int c = DEC ? cg : tf % TILE;
+        const bool second = DEC ? (threadIdx.x % T) == 1 : tf >= TILE;
         const long long rows = second ? g.rows_in2 : g.rows_in;
         const long long tail = second ? g.tail_in2 : g.tail_in;
         if ((PAIR || !second) && tail > 0 && rows < L1) {
@@ -255,11 +281,12 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
           }
         }
       }
-      __syncthreads();
+      bar();
     }
-    // ---- pass 0 from the landing boxes (interleaved mapping)
+    // ---- pass 0 from the landing boxes (interleaved mapping; DEC: the group's column)
     {
-      const int c = threadIdx.x % TILE, tp = threadIdx.x / TILE;
+      const int c = DEC ? cg : threadIdx.x % TILE;
+      const int tp = DEC ? (int)(threadIdx.x % T) : threadIdx.x / TILE;
       const int n2 = c0 + c;
       cplx *col = ex + c * CS;
       constexpr int S0 = PL::stride(0);
@@ -298,9 +325,21 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
       auto s_store = [&](int, int, int pos, cplx v) { col[fast::swz2(pos)] = v; };
       fast::pass<PL, 0, INV, false, R0, R0>(tp, a.ctw, tw0, in_load, s_store);
     }
-    __syncthreads();
+    bar();
     // the landing buffer is consumed: stream the next tile in behind the math
-    if (threadIdx.x == 0 && w + gridDim.x < ntiles) {
+    if constexpr (DEC) {
+      if (threadIdx.x % T == 0) {  // the last column group to get here refills
+        __threadfence_block();
+        if (atomicAdd(&land_rel, 1) == TILE - 1) {
+          land_rel = 0;
+          __threadfence_block();
+          if (w + gridDim.x < ntiles) {
+            tma::fence_proxy_async();
+            issue(w + gridDim.x);
+          }
+        }
+      }
+    } else if (threadIdx.x == 0 && w + gridDim.x < ntiles) {
       tma::fence_proxy_async();
       issue(w + gridDim.x);
     }
@@ -315,7 +354,7 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
       constexpr int q = decltype(qc)::value + 1;
       fast::pass<PL, q, INV, false, PL::radix[q], PL::radix[q], L1, true>(t, a.ctw, tw0, s_load,
                                                                          s_store);
-      __syncthreads();
+      bar();
     });
     // ST_C keeps only rows k < out_rows of y: when they fit in the first NOC
     // outputs of every last-pass butterfly (k = k0 + j L1/RL, j < NOC), the
@@ -326,7 +365,7 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
       fast::pass<PL, PL::P - 1, INV, false, RL, NOC, L1, true>(t, a.ctw, tw0, s_load, r_store);
     else
       fast::pass<PL, PL::P - 1, INV, false, RL, RL, L1, true>(t, a.ctw, tw0, s_load, r_store);
-    __syncthreads();
+    bar();
     // digit-reversed registers -> natural order: register j of butterfly beta
     // holds frequency k = k(beta) + j * L1 / RL; single-operand stage A also
     // applies the four-step twiddle W_L^{-+n2 k} (geometric in j)
@@ -362,7 +401,7 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
           col[nat(k)] = x;
       }
     }
-    __syncthreads();
+    bar();
     if (g.tma_out) {
       // ---- TMA-store epilogue
       if constexpr (PAIR) {
@@ -435,22 +474,22 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
         }
         wk = cmul(wk, wstep);
       }
-      __syncthreads();
+      bar();
       const int rows_out = a.out.e1;  // L1/2 + 1 with `half`, else L1
       // thread -> fixed column cc = tid % TILE, rows r0, r0 + NT/TILE, ...
       auto store_rows = [&](const Out2 &o) {
-        const int cc = threadIdx.x % TILE;
+        const int cc = DEC ? cg : threadIdx.x % TILE;
         if (c0 + cc >= a.L2) return;
-        constexpr int RS = NT / TILE;
+        constexpr int RS = DEC ? T : NT / TILE;
         const cplx *src = ex + cc * CS;
         cplx *d = static_cast<cplx *>(o.ptr) + item * o.item_stride + c0 + cc;
         const long long step = (long long)RS * o.s1;
-        int r = threadIdx.x / TILE;
+        int r = DEC ? (int)(threadIdx.x % T) : threadIdx.x / TILE;
         d += r * o.s1;
         for (; r < rows_out; r += RS, d += step) *d = src[nat(r)];
       };
       store_rows(a.out);
-      __syncthreads();
+      bar();
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
         const int k = t + p * T;
@@ -458,35 +497,35 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
         col[nat(k)] = xa[p];
         if (k != 0 && 2 * k != L1) col[nat(L1 - k)] = xb[p];
       }
-      __syncthreads();
+      bar();
       store_rows(a.out2);
     } else if constexpr (!SC) {
       const Out2 &o = a.out;
       const int rows = o.e1 < L1 ? o.e1 : L1;
-      const int cc = threadIdx.x % TILE;
+      const int cc = DEC ? cg : threadIdx.x % TILE;
       if (c0 + cc < o.e2) {
-        constexpr int RS = NT / TILE;
+        constexpr int RS = DEC ? T : NT / TILE;
         const cplx *src = ex + cc * CS;
-        int r = threadIdx.x / TILE;
+        int r = DEC ? (int)(threadIdx.x % T) : threadIdx.x / TILE;
         cplx *d = static_cast<cplx *>(o.ptr) + item * o.item_stride + c0 + cc + r * o.s1;
         for (; r < rows; r += RS, d += (long long)RS * o.s1) *d = src[nat(r)];
       }
     } else {
       // y(m2 + L2 k) for the rows k with m2 + L2 k < len
       const Out2 &o = a.out;
-      const int cc = threadIdx.x % TILE;
+      const int cc = DEC ? cg : threadIdx.x % TILE;
       if (c0 + cc < a.L2) {
         // rows r with (c0 + cc) + L2 r < len
         const long long krows = (o.len - (c0 + cc) + a.L2 - 1) / a.L2;
         const int rows = (int)(krows < L1 ? krows : L1);
-        constexpr int RS = NT / TILE;
+        constexpr int RS = DEC ? T : NT / TILE;
         const cplx *src = ex + cc * CS;
-        int r = threadIdx.x / TILE;
+        int r = DEC ? (int)(threadIdx.x % T) : threadIdx.x / TILE;
         cplx *d = static_cast<cplx *>(o.ptr) + item * o.item_stride + (c0 + cc) * o.s2 + r * o.s1;
         for (; r < rows; r += RS, d += (long long)RS * o.s1) *d = src[nat(r)];
       }
     }
-    __syncthreads();  // exchange buffer reused by the next tile's pass 0
+    bar();  // exchange buffer reused by the next tile's pass 0
   }
   if (g.tma_out && threadIdx.x == 0) tma::bulk_wait();
   tmem_fence_before();
@@ -529,8 +568,21 @@ static bool encode(CUtensorMap *m, const void *ptr, long long inner, long long r
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <class PL, int TILE, int STAGE, bool DEC>
+static cudaError_t launch_t2(ColTma &g, long long items, int ncols, cudaStream_t stream);
+
+// DEC (independent column groups, HK_COL_DEC=1) measured slower on B200 cfg3:
+// 433 vs 378 us -- per-column pass-0 reads of the packed landing rows and
+// per-column 16-byte row stores cost more than the CTA barriers they remove.
 template <class PL, int TILE, int STAGE>
 static cudaError_t launch_t(ColTma &g, long long items, int ncols, cudaStream_t stream) {
+  const bool dec = !g.tma_out && getenv("HK_COL_DEC") && atoi(getenv("HK_COL_DEC")) == 1;
+  return dec ? launch_t2<PL, TILE, STAGE, true>(g, items, ncols, stream)
+             : launch_t2<PL, TILE, STAGE, false>(g, items, ncols, stream);
+}
+
+template <class PL, int TILE, int STAGE, bool DEC>
+static cudaError_t launch_t2(ColTma &g, long long items, int ncols, cudaStream_t stream) {
   g.nat_swz = PL::L == 3072 ? 7 : 0;
   if (const char *e = getenv("HK_COL_NATSWZ")) g.nat_swz = atoi(e) & 7;
   using LY = TmaLayout<PL, TILE, STAGE>;
@@ -540,7 +592,7 @@ static cudaError_t launch_t(ColTma &g, long long items, int ncols, cudaStream_t 
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(configured.load() & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(k_cols_tma<PL, TILE, STAGE>,
+    cudaError_t e = cudaFuncSetAttribute(k_cols_tma<PL, TILE, STAGE, DEC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, LY::SMEM);
     if (e != cudaSuccess) return e;
     cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
@@ -550,7 +602,7 @@ static cudaError_t launch_t(ColTma &g, long long items, int ncols, cudaStream_t 
   const long long ntiles = (long long)tiles * items;
   if (ntiles <= 0) return cudaSuccess;
   const long long grid = std::min<long long>(ntiles, sms[dev & 63]);
-  k_cols_tma<PL, TILE, STAGE><<<(unsigned)grid, TILE * PL::T, LY::SMEM, stream>>>(g, tiles, ntiles);
+  k_cols_tma<PL, TILE, STAGE, DEC><<<(unsigned)grid, TILE * PL::T, LY::SMEM, stream>>>(g, tiles, ntiles);
   return cudaGetLastError();
 }
 
