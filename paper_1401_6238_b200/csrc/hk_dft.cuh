@@ -72,6 +72,11 @@ __device__ __forceinline__ float2 mul_pi(float2 a) { return make_float2(-a.y, a.
 
 template <bool INV, class C>
 __device__ __forceinline__ C cmul_dir(C a, C w) { return INV ? cmulc(a, w) : cmul(a, w); }
+// z^3 = a (a^2 - 3 b^2) + i b (3 a^2 - b^2): six FP64 instructions (two cmuls: eight)
+__device__ __forceinline__ cplx ccube(cplx z) {
+  const double a2 = z.x * z.x, b2 = z.y * z.y;
+  return make_double2(z.x * fma(-3.0, b2, a2), z.y * fma(3.0, a2, -b2));
+}
 
 // ---------------------------------------------------------------- constexpr twiddles
 // cos / sin of 2*pi*e/R computed at compile time: exact integer reduction to a
@@ -345,6 +350,55 @@ __device__ __forceinline__ void stage2(const C (&t)[16], C *v) {
     v[k1 + 4] = axpy<s1, 1>(t1, df);
     v[k1 + 12] = axpy<s1, -1>(t1, df);
   });
+}
+
+// Column-major twiddle chunks of a radix-16 butterfly: chunk c holds the
+// input twiddles of stage-1 column n2 = c, i.e. j = c + 4q (q = 0..3; chunk 0
+// holds j = 4, 8, 12 and one pad).  0 marks the pad slot.
+constexpr int colj(int c, int q) { return c == 0 ? (q < 3 ? 4 * (q + 1) : 0) : c + 4 * q; }
+
+// q + x * w (INV: q + x * conj w) in four FMAs
+template <bool INV, class C>
+__device__ __forceinline__ C cfma_dir(C q, C x, C w) {
+  if constexpr (INV)
+    return CT<C>::make(fma(x.x, w.x, fma(x.y, w.y, q.x)), fma(x.y, w.x, fma(-x.x, w.y, q.y)));
+  else
+    return CT<C>::make(fma(x.x, w.x, fma(-x.y, w.y, q.x)), fma(x.x, w.y, fma(x.y, w.x, q.y)));
+}
+// 2 q - s (the difference partner of s = q + d, one FMA per component)
+template <class C>
+__device__ __forceinline__ C twice_minus(C q, C s) {
+  using S = typename CT<C>::S;
+  return CT<C>::make(fma((S)2, q.x, -s.x), fma((S)2, q.y, -s.y));
+}
+
+// Radix-16 with input twiddles v[j] *= w_j (j = 1..15) folded into the first
+// radix-4 stage (the transposed-DIT passes of the final transform):
+//   x0 + w2 x2 = four FMAs, x0 - w2 x2 = 2 x0 - (x0 + w2 x2) = two more,
+// so a twiddled column costs 24-28 FP64 instructions instead of 28-32.
+// getw(c, w) loads chunk c in the colj layout.
+template <bool INV, class C, class GetW>
+__device__ __forceinline__ void dft16_tw_in(C (&v)[16], GetW &&getw) {
+  C t[16];
+  sfor<4>([&](auto n2c) {
+    constexpr int n2 = decltype(n2c)::value;
+    C w[4];
+    getw(n2, w);
+    // x_n1 = v[4 n1 + n2] carries twiddle j = 4 n1 + n2 = w[n2 ? n1 : n1 - 1]
+    const C q0 = n2 == 0 ? v[n2] : cmul_dir<INV>(v[n2], w[0]);
+    const C w1 = w[n2 ? 1 : 0], w2 = w[n2 ? 2 : 1], w3 = w[n2 ? 3 : 2];
+    const C s0 = cfma_dir<INV>(q0, v[8 + n2], w2);
+    const C s1 = twice_minus(q0, s0);
+    const C p = cmul_dir<INV>(v[4 + n2], w1);
+    const C s2 = cfma_dir<INV>(p, v[12 + n2], w3);
+    C s3 = twice_minus(p, s2);
+    s3 = INV ? mul_pi(s3) : mul_mi(s3);
+    t[0 * 4 + n2] = cadd(s0, s2);
+    t[2 * 4 + n2] = csub(s0, s2);
+    t[1 * 4 + n2] = cadd(s1, s3);
+    t[3 * 4 + n2] = csub(s1, s3);
+  });
+  stage2<INV>(t, v);
 }
 }  // namespace r16
 

@@ -126,6 +126,13 @@ template <class T, class = void>
 struct HasChunk1 : std::false_type {};
 template <class T>
 struct HasChunk1<T, std::void_t<decltype(&T::chunk1)>> : std::true_type {};
+// Sources with kColChunks store a butterfly's twiddles in the column-major
+// chunk order of r16::colj (chunk c = stage-1 column c of the radix-16), so the
+// final transform's twiddled passes fold them into the first radix-4 stage.
+template <class T, class = void>
+struct ColChunks : std::false_type {};
+template <class T>
+struct ColChunks<T, std::void_t<decltype(T::kColChunks)>> : std::bool_constant<T::kColChunks> {};
 
 // Pass-0 twiddles by recurrence: W_L^{j beta} = (W_L^beta)^j from one table
 // read per butterfly (two interleaved chains, <= 8 products deep), trading
@@ -193,6 +200,11 @@ __device__ __forceinline__ void pass(int t, const C *__restrict__ tw, const TW0 
   constexpr bool HIM = Tr::hi_major(p) && !HasChunk1<TW0>::value;
   constexpr int NIN = FINAL ? R : NZ;
   constexpr int NOUT = NO;  // DIF passes: NO < R prunes outputs (callers pass R otherwise)
+  constexpr bool kCol = ColChunks<TW0>::value;
+  static_assert(!kCol || R == 16 || (p != 0 && !(p == 1 && PL::P == 3)),
+                "column-major twiddle chunks are laid out for radix-16 passes");
+  constexpr bool kFuse = FINAL && kCol && R == 16 && PL::P == 3 && (p == 0 || p == 1) &&
+                         ChunkOf<TW0>::value == 4 && !is_tw0rec<TW0>::value;
   // Pass-0 recurrence bases of a thread's NB butterflies, beta = t + i*T:
   // W_L^beta = W_L^t * W_L^{i T}, the second factor a compile-time constant,
   // so one table read serves all NB butterflies (8192 = 2 x 16^3: NB = 8).
@@ -272,8 +284,9 @@ __device__ __forceinline__ void pass(int t, const C *__restrict__ tw, const TW0 
             C w[CK];
             tw0.chunk(beta, c, w);
             sfor<CK>([&](auto qc) {
-              constexpr int j = CK * c + decltype(qc)::value + 1;
-              if constexpr (j < R) a[j] = cmul_dir<INV>(a[j], w[decltype(qc)::value]);
+              constexpr int q = decltype(qc)::value;
+              constexpr int j = kCol ? r16::colj(c, q) : CK * c + q + 1;
+              if constexpr (j > 0 && j < R) a[j] = cmul_dir<INV>(a[j], w[q]);
             });
           });
         } else if constexpr (p == 1 && PL::P == 3 && HasChunk1<TW0>::value) {
@@ -282,8 +295,9 @@ __device__ __forceinline__ void pass(int t, const C *__restrict__ tw, const TW0 
             C w[4];
             tw0.chunk1(c, w);
             sfor<4>([&](auto qc) {
-              constexpr int j = 4 * c + decltype(qc)::value + 1;
-              if constexpr (j < R) a[j] = cmul_dir<INV>(a[j], w[decltype(qc)::value]);
+              constexpr int q = decltype(qc)::value;
+              constexpr int j = kCol ? r16::colj(c, q) : 4 * c + q + 1;
+              if constexpr (j > 0 && j < R) a[j] = cmul_dir<INV>(a[j], w[q]);
             });
           });
         } else if constexpr (p < PL::P - 1 && REC) {
@@ -306,7 +320,15 @@ __device__ __forceinline__ void pass(int t, const C *__restrict__ tw, const TW0 
           });
         }
       };
-      if constexpr (FINAL) {
+      if constexpr (kFuse) {
+        // input twiddles folded into the first radix-4 stage (r16::dft16_tw_in)
+        r16::dft16_tw_in<false>(a, [&](int c, C *w) {
+          if constexpr (p == 0)
+            tw0.chunk(beta, c, w);
+          else
+            tw0.chunk1(c, w);
+        });
+      } else if constexpr (FINAL) {
         twiddle();
         DftP<R, false, R, NO>::run(a);
       } else {

@@ -111,7 +111,11 @@ struct Tw0Tmem8 {
 // Both twiddle sets from TMEM: pass 0 (W_L^{j t}) and pass 1 (W_{L/R0}^{j lo}).
 // A thread's twiddles depend only on its index in its group, so the two
 // groups' warps that share a TMEM lane quadrant and an index share one slab.
-struct Tw01Tmem {
+// COL: chunks in the column-major order of r16::colj (the final transform then
+// folds them into its first radix-4 stage, fast::pass kFuse).
+template <bool COL>
+struct Tw01TmemT {
+  static constexpr bool kColChunks = COL;
   uint32_t taddr0, taddr1;
   __device__ __forceinline__ void chunk(int, int c, cplx *w) const { tmem_ld4(taddr0 + 16 * c, w); }
   __device__ __forceinline__ void chunk1(int c, cplx *w) const { tmem_ld4(taddr1 + 16 * c, w); }
@@ -189,6 +193,9 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
   const uint32_t lane_q = (uint32_t)(32 * (warp & 3)) << 16;
   const uint32_t tacc = tmem_slot + lane_q + (uint32_t)((warp >> 2) * 64);
   constexpr bool TW1T = (TWV & 8) != 0;
+  // TWV bit 7: column-major twiddle chunks, folded into the final transform's
+  // first radix-4 stages; and the cube X^3 in six FP64 instructions
+  constexpr bool COLW = TW1T && (TWV & 128) != 0;
   // with TW1T the pass-0 slab of the thread index t_in is shared by both groups
   // (cols 256 + 64 * ((warp >> 2) & 1)) and the pass-1 slab sits at 384 + ...
   const uint32_t ttw = tmem_slot + lane_q + 256u +
@@ -203,10 +210,19 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
       // fast::pass): lo = t mod stride(1), twiddles W_{L/R0}^{j lo}
       constexpr int R1 = PL::radix[1];
       const int lo1 = t_in % PL::stride(1);
+      static_assert(!COLW || (R0 == 16 && PL::radix[1] == 16), "column chunks: radix-16 passes");
 #pragma unroll
       for (int c = 0; c < (R0 - 1 + 3) / 4; ++c) {
         cplx w[4];
-        g0.chunk(t_in, c, w);
+        if constexpr (COLW) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int j = r16::colj(c, q);
+            w[q] = j > 0 ? a.tw0[(j - 1) * (L / R0) + t_in] : make_double2(1.0, 0.0);
+          }
+        } else {
+          g0.chunk(t_in, c, w);
+        }
         tmem_st4(ttw + 16 * c, w);
       }
 #pragma unroll
@@ -214,8 +230,8 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
         cplx w[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int j = 4 * c + q + 1;
-          w[q] = j < R1 ? a.tw1[(j * lo1) % TW1] : make_double2(1.0, 0.0);
+          const int j = COLW ? r16::colj(c, q) : 4 * c + q + 1;
+          w[q] = (j > 0 && j < R1) ? a.tw1[(j * lo1) % TW1] : make_double2(1.0, 0.0);
         }
         tmem_st4(ttw1 + 16 * c, w);
       }
@@ -236,12 +252,12 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
     tmem_wait_st();
   }
   using TW0 = std::conditional_t<
-      TW1T, Tw01Tmem,
+      TW1T, Tw01TmemT<COLW>,
       std::conditional_t<(TWV & 1) != 0, fast::Tw0Rec,
                          std::conditional_t<(TWV & 4) != 0, Tw0Tmem8, Tw0Tmem>>>;
   TW0 tw0;
   if constexpr (TW1T)
-    tw0 = Tw01Tmem{ttw, ttw1};
+    tw0 = TW0{ttw, ttw1};
   else if constexpr ((TWV & 1) != 0)
     tw0 = fast::Tw0Rec{a.tw};
   else
@@ -407,9 +423,14 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp(const __grid_constan
       for (int c = 0; c < V / 4; ++c) {
         cplx acc[4];
         tmem_ld4(tacc + 16 * c, acc);
-        for (int q = 0; q < a.fac[0].power; ++q) {
+        if (COLW && a.fac[0].power == 3) {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) acc[e] = cmul(acc[e], v[4 * c + e]);
+          for (int e = 0; e < 4; ++e) acc[e] = cmul(acc[e], ccube(v[4 * c + e]));
+        } else {
+          for (int q = 0; q < a.fac[0].power; ++q) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[e] = cmul(acc[e], v[4 * c + e]);
+          }
         }
 #pragma unroll
         for (int e = 0; e < 4; ++e) v[4 * c + e] = acc[e];
@@ -723,13 +744,17 @@ cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream) {
   constexpr int s0 = PL::stride(0);
   const int nz = (x.len + s0 - 1) / s0, no = (a.out_len + s0 - 1) / s0;
   // 24: TMEM pass-0 and pass-1 twiddles + split WAR barriers (r02: 169.4 us vs
-  // 170.0 for 8 and 185.6 for 2 = recurrence for pass 1, the r01 default)
-  int twv = 24;
-  if (const char *e = getenv("HK_PP_TWV")) twv = atoi(e) & 127;
+  // 170.0 for 8 and 185.6 for 2 = recurrence for pass 1, the r01 default);
+  // +128: column-major twiddle chunks folded into the final transform's first
+  // radix-4 stages, cube in six instructions (HK_PP_COLW=0 turns it off)
+  const bool colw = !(getenv("HK_PP_COLW") && atoi(getenv("HK_PP_COLW")) == 0);
+  int twv = colw ? 152 : 24;
+  if (const char *e = getenv("HK_PP_TWV")) twv = atoi(e) & 255;
   if (nz == 16 && !getenv("HK_NO_PP_ROWS")) {  // full rows (two-level row stage)
     const bool one = getenv("HK_PP_ROWS_TWO") == nullptr;  // A/B: two code copies
-    if (no <= 4) return one ? pp::launch_pp<PL, 16, 4, 56>(a, stream) : pp::launch_pp<PL, 16, 4, 24>(a, stream);
-    return one ? pp::launch_pp<PL, 16, 16, 56>(a, stream) : pp::launch_pp<PL, 16, 16, 24>(a, stream);
+    if (!one) return no <= 4 ? pp::launch_pp<PL, 16, 4, 24>(a, stream) : pp::launch_pp<PL, 16, 16, 24>(a, stream);
+    if (colw) return no <= 4 ? pp::launch_pp<PL, 16, 4, 184>(a, stream) : pp::launch_pp<PL, 16, 16, 184>(a, stream);
+    return no <= 4 ? pp::launch_pp<PL, 16, 4, 56>(a, stream) : pp::launch_pp<PL, 16, 16, 56>(a, stream);
   }
   if (nz <= 4 && no <= 4 && a.nsub == 1) {
     switch (twv) {
@@ -737,11 +762,8 @@ cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream) {
       case 24: return pp::launch_pp<PL, 4, 4, 24>(a, stream);
       case 56: return pp::launch_pp<PL, 4, 4, 56>(a, stream);
       case 88: return pp::launch_pp<PL, 4, 4, 88>(a, stream);
-      case 6: return pp::launch_pp<PL, 4, 4, 6>(a, stream);
-      case 1: return pp::launch_pp<PL, 4, 4, 1>(a, stream);
-      case 2: return pp::launch_pp<PL, 4, 4, 2>(a, stream);
-      case 3: return pp::launch_pp<PL, 4, 4, 3>(a, stream);
-      default: return pp::launch_pp<PL, 4, 4, 0>(a, stream);
+      case 152: return pp::launch_pp<PL, 4, 4, 152>(a, stream);
+      default: return pp::launch_pp<PL, 4, 4, 2>(a, stream);
     }
   }
   return cudaErrorNotSupported;  // x staging would not fit next to three L buffers

@@ -101,7 +101,7 @@ def test_bhhb_fused_cfg4_golden(monkeypatch):
     np.testing.assert_allclose(np.linalg.norm(y, axis=1), g["norms"][:160], rtol=TOL)
 
 
-@pytest.mark.parametrize("twv", ["2", "8", "24", "56"])
+@pytest.mark.parametrize("twv", ["2", "8", "24", "56", "152"])
 def test_cfg2_kernel_variants(monkeypatch, twv):
     monkeypatch.setenv("HK_PP_TWV", twv)
     g = load_golden("cfg2.npz")
