@@ -87,32 +87,71 @@ __global__ void __launch_bounds__(TILE * PL::T, (col_blocks<PL, TILE>())) k_cols
   const int c = threadIdx.x / T, t = threadIdx.x - (threadIdx.x / T) * T;
   const bool real_in = a.in.kind == FK_F64;
 
+  // Rows of column n2 that exist in an operand / output: 1D layout (len >= 0)
+  // element (n1, n2) is n2 + L2 n1 < len, i.e. n1 < len / L2 + (n2 < len % L2);
+  // 2D layout: n1 < e1 for n2 < e2.  The 64-bit divisions run once per thread.
+  struct Lim {
+    int q, rem, e2;  // rows = n2 < e2 ? q + (n2 < rem) : 0
+    __device__ __forceinline__ int rows(int n2) const { return n2 < e2 ? q + (n2 < rem ? 1 : 0) : 0; }
+  };
+  auto make_lim = [&](long long len, int e1, int e2) {
+    if (len >= 0) {
+      const long long q = len / a.L2;
+      return Lim{(int)(q < L1 ? q : L1), q < L1 ? (int)(len - q * a.L2) : 0, a.L2};
+    }
+    return Lim{e1 < L1 ? e1 : L1, 0, e2};
+  };
+  const Lim lim_in = make_lim(a.in.len, a.in.e1, a.in.e2);
+  const Lim lim_in2 = PAIR ? make_lim(a.in2.len, a.in2.e1, a.in2.e2) : Lim{0, 0, 0};
+  const Lim lim_out = make_lim(a.out.len, a.out.e1, a.out.e2);
+  const Lim lim_out2 = PAIR ? make_lim(a.out2.len, a.out2.e1, a.out2.e2) : Lim{0, 0, 0};
+
+  // Tile load.  r02 ncu (cfg4 h pass): the per-element index arithmetic of the
+  // generic loop (runtime divisions, 64-bit bounds and three 64-bit multiplies
+  // per element, ~40 integer instructions) was 35% of the kernel.  Here the
+  // loop is unrolled with compile-time element indices, the bounds are one
+  // integer compare, and the address is base + n1 s1 + n2 s2.
+  constexpr int NI = (TILE * L1 + NT - 1) / NT;
   auto issue = [&](long long w, cplx *tile) {
     const long long item = w / tiles_per_item;
     const int c0 = (int)(w - item * tiles_per_item) * TILE;
-    for (int idx = threadIdx.x; idx < TILE * L1; idx += NT) {
-      const int cc = a.in_n1_fast ? idx / L1 : idx % TILE;
-      const int n1d = a.in_n1_fast ? idx - (idx / L1) * L1 : idx / TILE;
+    const bool half_c = STAGE == ST_C && a.half;
+    const int esz = real_in || PAIR ? 8 : 16;
+    const char *b1 = static_cast<const char *>(a.in.ptr) + item * a.in.item_stride * esz;
+    const char *b2 = PAIR ? static_cast<const char *>(a.in2.ptr) + item * a.in2.item_stride * 8
+                          : nullptr;
+    auto one = [&](int cc, int n1d) {
       // Hermitian half (ST_C): rows above L1/2 are read from row L1 - n1
-      const int n1 = (STAGE == ST_C && a.half && 2 * n1d > L1) ? L1 - n1d : n1d;
+      const int n1 = (half_c && 2 * n1d > L1) ? L1 - n1d : n1d;
       const int n2 = c0 + cc;
-      bool ok;
-      if (a.in.len >= 0)
-        ok = n2 < a.L2 && (long long)n2 + (long long)a.L2 * n1 < a.in.len;
-      else
-        ok = n1 < a.in.e1 && n2 < a.in.e2;
-      const long long off = ok ? item * a.in.item_stride + n1 * a.in.s1 + n2 * a.in.s2 : 0;
+      const bool ok = n1 < lim_in.rows(n2);
+      const long long off = ok ? n1 * a.in.s1 + n2 * a.in.s2 : 0;
       const uint32_t dst = smem_u32(tile + cc * CS + fast::swz2(n1d));
       if constexpr (PAIR) {  // z = h + i x from two real streams (1D layout)
-        const bool ok2 = n2 < a.L2 && (long long)n2 + (long long)a.L2 * n1 < a.in2.len;
-        const long long off2 =
-            ok2 ? item * a.in2.item_stride + n1 * a.in2.s1 + n2 * a.in2.s2 : 0;
-        cp_async8(dst, static_cast<const double *>(a.in.ptr) + off, ok);
-        cp_async8(dst + 8, static_cast<const double *>(a.in2.ptr) + off2, ok2);
+        const bool ok2 = n1 < lim_in2.rows(n2);
+        const long long off2 = ok2 ? n1 * a.in2.s1 + n2 * a.in2.s2 : 0;
+        cp_async8(dst, b1 + off * 8, ok);
+        cp_async8(dst + 8, b2 + off2 * 8, ok2);
       } else if (real_in) {
-        cp_async8(dst, static_cast<const double *>(a.in.ptr) + off, ok);
+        cp_async8(dst, b1 + off * 8, ok);
       } else {
-        cp_async16(dst, static_cast<const cplx *>(a.in.ptr) + off, ok);
+        cp_async16(dst, b1 + off * 16, ok);
+      }
+    };
+    if (a.in_n1_fast) {
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        const int idx = (int)threadIdx.x + i * NT;
+        if ((TILE * L1) % NT != 0 && idx >= TILE * L1) break;
+        const int cc = idx / L1;
+        one(cc, idx - cc * L1);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        const int idx = (int)threadIdx.x + i * NT;
+        if ((TILE * L1) % NT != 0 && idx >= TILE * L1) break;
+        one(idx % TILE, idx / TILE);
       }
     }
     cp_async_commit();
@@ -215,18 +254,16 @@ __global__ void __launch_bounds__(TILE * PL::T, (col_blocks<PL, TILE>())) k_cols
     }
     __syncthreads();
     // coalesced tile store
-    auto store_tile = [&](const Out2 &o) {
-      for (int idx = threadIdx.x; idx < TILE * L1; idx += NT) {
-        const int cc = idx % TILE, n1 = idx / TILE, m2 = c0 + cc;
-        bool ok;
-        if (o.len >= 0)
-          ok = m2 < a.L2 && (long long)m2 + (long long)a.L2 * n1 < o.len;
-        else
-          ok = n1 < o.e1 && m2 < o.e2;
-        if (ok)
-          static_cast<cplx *>(o.ptr)[item * o.item_stride + n1 * o.s1 + m2 * o.s2] =
-              tile[cc * CS + n1];
-      }
+    auto store_tile = [&](const Out2 &o, const Lim &lim) {
+      // thread -> fixed column cc = tid % TILE, rows tid / TILE + i (NT / TILE)
+      const int cc = threadIdx.x % TILE, m2 = c0 + cc;
+      const int rows = lim.rows(m2);
+      int n1 = threadIdx.x / TILE;
+      cplx *d = static_cast<cplx *>(o.ptr) + item * o.item_stride + n1 * o.s1 + m2 * o.s2;
+      const long long step = (long long)(NT / TILE) * o.s1;
+      const cplx *src = tile + cc * CS;
+#pragma unroll 4
+      for (; n1 < rows; n1 += NT / TILE, d += step) *d = src[n1];
     };
     if constexpr (PAIR) {
       // col[k] = Z(k) = H(k) + i X(k) with H, X the column DFTs of the real
@@ -258,7 +295,7 @@ __global__ void __launch_bounds__(TILE * PL::T, (col_blocks<PL, TILE>())) k_cols
         if (kk != k) col[kk] = make_double2(hkk.x * sh, hkk.y * sh);
       }
       __syncthreads();
-      store_tile(a.out);
+      store_tile(a.out, lim_out);
       __syncthreads();
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
@@ -268,9 +305,9 @@ __global__ void __launch_bounds__(TILE * PL::T, (col_blocks<PL, TILE>())) k_cols
         if (k != 0 && 2 * k != L1) col[L1 - k] = xb[p];  // kk == k for k = 0, L1/2
       }
       __syncthreads();
-      store_tile(a.out2);
+      store_tile(a.out2, lim_out2);
     } else {
-      store_tile(a.out);
+      store_tile(a.out, lim_out);
     }
     __syncthreads();  // this buffer is refilled two iterations later
   }
