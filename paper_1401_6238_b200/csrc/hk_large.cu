@@ -111,7 +111,20 @@ __global__ void __launch_bounds__(TILE * PL::T, (col_blocks<PL, TILE>())) k_cols
   // per element, ~40 integer instructions) was 35% of the kernel.  Here the
   // loop is unrolled with compile-time element indices, the bounds are one
   // integer compare, and the address is base + n1 s1 + n2 s2.
-  constexpr int NI = (TILE * L1 + NT - 1) / NT;
+  // Element i of a thread is idx = tid + i NT of the TILE x L1 tile (NI = V of
+  // them).  Operand contiguous along n1 (in_n1_fast): idx = cc L1 + n1d; else
+  // idx = n1d TILE + cc.  NT divides L1 or L1 divides NT (NT = TILE L1 / V, TILE
+  // and V powers of two... or equal), so the split of idx is a per-thread
+  // constant plus a compile-time function of i; item-relative offsets are
+  // 32-bit (launch_cols_t checks the extent).
+  constexpr int NI = (TILE * L1) / NT;
+  static_assert(NI * NT == TILE * L1 && NT % TILE == 0, "whole tile per pass of the CTA");
+  constexpr bool kSplit = L1 % NT == 0 || NT % L1 == 0;
+  const int f_cc0 = kSplit ? (L1 % NT == 0 ? 0 : (int)threadIdx.x / L1) : 0;
+  const int f_n0 = kSplit ? (L1 % NT == 0 ? (int)threadIdx.x : (int)threadIdx.x % L1) : 0;
+  const int s_cc = threadIdx.x % TILE, s_n0 = threadIdx.x / TILE;
+  const uint32_t is1 = (uint32_t)a.in.s1, is2 = (uint32_t)a.in.s2;
+  const uint32_t is1b = PAIR ? (uint32_t)a.in2.s1 : 0u, is2b = PAIR ? (uint32_t)a.in2.s2 : 0u;
   auto issue = [&](long long w, cplx *tile) {
     const long long item = w / tiles_per_item;
     const int c0 = (int)(w - item * tiles_per_item) * TILE;
@@ -120,39 +133,51 @@ __global__ void __launch_bounds__(TILE * PL::T, (col_blocks<PL, TILE>())) k_cols
     const char *b1 = static_cast<const char *>(a.in.ptr) + item * a.in.item_stride * esz;
     const char *b2 = PAIR ? static_cast<const char *>(a.in2.ptr) + item * a.in2.item_stride * 8
                           : nullptr;
-    auto one = [&](int cc, int n1d) {
+    auto one = [&](int cc, int n1d, int rows, int rows2) {
       // Hermitian half (ST_C): rows above L1/2 are read from row L1 - n1
       const int n1 = (half_c && 2 * n1d > L1) ? L1 - n1d : n1d;
-      const int n2 = c0 + cc;
-      const bool ok = n1 < lim_in.rows(n2);
-      const long long off = ok ? n1 * a.in.s1 + n2 * a.in.s2 : 0;
+      const uint32_t n2 = (uint32_t)(c0 + cc);
+      const bool ok = n1 < rows;
+      const uint32_t off = ok ? (uint32_t)n1 * is1 + n2 * is2 : 0u;
       const uint32_t dst = smem_u32(tile + cc * CS + fast::swz2(n1d));
       if constexpr (PAIR) {  // z = h + i x from two real streams (1D layout)
-        const bool ok2 = n1 < lim_in2.rows(n2);
-        const long long off2 = ok2 ? n1 * a.in2.s1 + n2 * a.in2.s2 : 0;
-        cp_async8(dst, b1 + off * 8, ok);
-        cp_async8(dst + 8, b2 + off2 * 8, ok2);
+        const bool ok2 = n1 < rows2;
+        const uint32_t off2 = ok2 ? (uint32_t)n1 * is1b + n2 * is2b : 0u;
+        cp_async8(dst, b1 + (size_t)off * 8, ok);
+        cp_async8(dst + 8, b2 + (size_t)off2 * 8, ok2);
       } else if (real_in) {
-        cp_async8(dst, b1 + off * 8, ok);
+        cp_async8(dst, b1 + (size_t)off * 8, ok);
       } else {
-        cp_async16(dst, b1 + off * 16, ok);
+        cp_async16(dst, b1 + (size_t)off * 16, ok);
       }
     };
     if (a.in_n1_fast) {
+      if constexpr (L1 % NT == 0) {  // a column spans K = L1 / NT passes
+        constexpr int K = L1 / NT;
 #pragma unroll
-      for (int i = 0; i < NI; ++i) {
-        const int idx = (int)threadIdx.x + i * NT;
-        if ((TILE * L1) % NT != 0 && idx >= TILE * L1) break;
-        const int cc = idx / L1;
-        one(cc, idx - cc * L1);
+        for (int cc = 0; cc < TILE; ++cc) {
+          const int rows = lim_in.rows(c0 + cc), rows2 = PAIR ? lim_in2.rows(c0 + cc) : 0;
+#pragma unroll
+          for (int k = 0; k < K; ++k) one(cc, f_n0 + k * NT, rows, rows2);
+        }
+      } else if constexpr (NT % L1 == 0) {  // M = NT / L1 columns per pass
+        constexpr int M = NT / L1;
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          const int cc = i * M + f_cc0;
+          one(cc, f_n0, lim_in.rows(c0 + cc), PAIR ? lim_in2.rows(c0 + cc) : 0);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          const int idx = (int)threadIdx.x + i * NT, cc = idx / L1;
+          one(cc, idx - cc * L1, lim_in.rows(c0 + cc), PAIR ? lim_in2.rows(c0 + cc) : 0);
+        }
       }
     } else {
+      const int rows = lim_in.rows(c0 + s_cc), rows2 = PAIR ? lim_in2.rows(c0 + s_cc) : 0;
 #pragma unroll
-      for (int i = 0; i < NI; ++i) {
-        const int idx = (int)threadIdx.x + i * NT;
-        if ((TILE * L1) % NT != 0 && idx >= TILE * L1) break;
-        one(idx % TILE, idx / TILE);
-      }
+      for (int i = 0; i < NI; ++i) one(s_cc, s_n0 + i * (NT / TILE), rows, rows2);
     }
     cp_async_commit();
   };
@@ -255,15 +280,25 @@ __global__ void __launch_bounds__(TILE * PL::T, (col_blocks<PL, TILE>())) k_cols
     __syncthreads();
     // coalesced tile store
     auto store_tile = [&](const Out2 &o, const Lim &lim) {
-      // thread -> fixed column cc = tid % TILE, rows tid / TILE + i (NT / TILE)
-      const int cc = threadIdx.x % TILE, m2 = c0 + cc;
+      // thread -> fixed column cc = tid % TILE, rows tid / TILE + i (NT / TILE),
+      // i < NI; the shared-memory reads of half a tile are issued before its stores
+      const int m2 = c0 + s_cc;
       const int rows = lim.rows(m2);
-      int n1 = threadIdx.x / TILE;
-      cplx *d = static_cast<cplx *>(o.ptr) + item * o.item_stride + n1 * o.s1 + m2 * o.s2;
+      cplx *d = static_cast<cplx *>(o.ptr) + item * o.item_stride + s_n0 * o.s1 + m2 * o.s2;
       const long long step = (long long)(NT / TILE) * o.s1;
-      const cplx *src = tile + cc * CS;
-#pragma unroll 4
-      for (; n1 < rows; n1 += NT / TILE, d += step) *d = src[n1];
+      const cplx *src = tile + s_cc * CS + s_n0;
+      constexpr int NB = NI >= 8 ? 8 : NI;
+#pragma unroll
+      for (int i0 = 0; i0 < NI; i0 += NB) {
+        if (s_n0 + i0 * (NT / TILE) >= rows) break;
+        cplx u[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i)
+          if (i0 + i < NI && s_n0 + (i0 + i) * (NT / TILE) < rows) u[i] = src[(i0 + i) * (NT / TILE)];
+#pragma unroll
+        for (int i = 0; i < NB; ++i)
+          if (i0 + i < NI && s_n0 + (i0 + i) * (NT / TILE) < rows) d[(i0 + i) * step] = u[i];
+      }
     };
     if constexpr (PAIR) {
       // col[k] = Z(k) = H(k) + i X(k) with H, X the column DFTs of the real
@@ -354,6 +389,12 @@ static cudaError_t launch_cols_t(const ColArgs &a, long long items, int ncols,
     resident[dev & 63] = sms * std::max(1, per);
     configured.fetch_or(bit);
   }
+  // the tile loads address operands with 32-bit item-relative element offsets
+  auto small = [&](const Op2 &op) {
+    return op.s1 >= 0 && op.s2 >= 0 &&
+           (long long)(PL::L - 1) * op.s1 + (long long)(a.L2 + TILE) * op.s2 < (1ll << 31);
+  };
+  if (!small(a.in) || (STAGE == ST_A_PAIR && !small(a.in2))) return cudaErrorNotSupported;
   const int tiles = (ncols + TILE - 1) / TILE;
   const long long ntiles = (long long)tiles * items;
   if (ntiles <= 0) return cudaSuccess;
