@@ -46,7 +46,6 @@ struct alignas(64) ColTma {
   int32_t tma_out;              // 1: epilogue stores the tile with TMA (row-major staging)
   int32_t out_rows;             // rows of the output tile (stage A: e1; ST_C: len / L2)
   int32_t nat_swz;              // natural-order column layout: k ^ ((k >> 3) & nat_swz)
-  int32_t wide_out;             // 1: 32-byte row stores (column pairs), see store_pairs
   int32_t nb_in, nb_in2;        // landing boxes that hold operand rows (the rest stay zero)
   int32_t fb_in, fb_in2;        // of which full 256-row blocks (one 4-D copy; < nb: one more box)
   long long c_q, c_rem;         // ST_C: out.len = c_q * L2 + c_rem
@@ -121,12 +120,6 @@ struct GroupBar {
 __device__ __forceinline__ cplx tw4(const ColArgs &a, long long e) {
   if (e >= a.L) e -= a.L;
   return cmul(__ldg(&a.thi[e >> 12]), __ldg(&a.tlo[e & 4095]));
-}
-// one thread stores 32 contiguous bytes (two complex128 columns of a row)
-__device__ __forceinline__ void st256(cplx *d, cplx v0, cplx v1) {
-  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(d), "d"(v0.x), "d"(v0.y),
-               "d"(v1.x), "d"(v1.y)
-               : "memory");
 }
 
 // Column-pass twiddles in TMEM (r02): a thread's twiddles are the same for
@@ -297,6 +290,23 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
 
   for (int it = 0; w < ntiles; ++it, w += gridDim.x, next_tile(item, tcol)) {
     const int c0 = tcol * TILE;
+    // ST_C: the four-step twiddles of this thread's pass-0 butterflies (table
+    // reads that miss L1 next to 197 KB of shared memory) are requested before
+    // the wait for the tile, not between the wait and the first butterfly
+    constexpr int NB0 = ColTw<PL>::NB0;
+    cplx pz_step = make_double2(1.0, 0.0), pz_row = pz_step, pz_cur[NB0];
+    if constexpr (SC) {
+      const int c = DEC ? cg : threadIdx.x % TILE;
+      const int tp = DEC ? (int)(threadIdx.x % T) : threadIdx.x / TILE;
+      const int n2 = c0 + c;
+      pz_step = tw4(a, (long long)n2 * PL::stride(0));
+      if (a.half) pz_row = tw4(a, (long long)n2 * L1);  // W_L2^{n2}
+#pragma unroll
+      for (int i = 0; i < NB0; ++i) {
+        const int beta = tp + i * T;
+        pz_cur[i] = beta < L1 / R0 ? tw4(a, (long long)n2 * beta) : pz_step;
+      }
+    }
     tma::mbar_wait(mb, (uint32_t)(it & 1));
     if (g.tma_out) {  // the previous tile's TMA stores have read the exchange buffer
       if (threadIdx.x == 0) tma::bulk_wait_read();
@@ -331,15 +341,10 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
     {
       const int c = DEC ? cg : threadIdx.x % TILE;
       const int tp = DEC ? (int)(threadIdx.x % T) : threadIdx.x / TILE;
-      const int n2 = c0 + c;
       cplx *col = ex + c * CS;
-      constexpr int S0 = PL::stride(0);
-      cplx tw_cur = make_double2(1.0, 0.0), tw_step = make_double2(1.0, 0.0), wrow = tw_step;
-      if constexpr (SC) {
-        tw_step = tw4(a, (long long)n2 * S0);
-        if (a.half) wrow = tw4(a, (long long)n2 * L1);  // W_L2^{n2}
-      }
-      auto in_load = [&](int, int j, int pos) {
+      cplx tw_cur = make_double2(1.0, 0.0);
+      const cplx tw_step = pz_step, wrow = pz_row;
+      auto in_load = [&](int i, int j, int pos) {
         if constexpr (PAIR) {
           return make_double2(land[pos * TILE + c], land[(L1 + pos) * TILE + c]);
         } else if constexpr (!SC) {
@@ -360,7 +365,7 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
           }
           v.x *= a.in.scale;
           v.y *= a.in.scale;
-          if (j == 0) tw_cur = tw4(a, (long long)n2 * pos);
+          if (j == 0) tw_cur = pz_cur[i];  // W_L^{n2 beta}: pos = beta + j S0
           v = cmul(v, tw_cur);
           tw_cur = cmul(tw_cur, tw_step);
           return v;
@@ -421,36 +426,6 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
     // digit-reversed writes at L1 = 3072: 8 wavefronts per warp store -> 4)
     const int nswz = g.nat_swz;
     auto nat = [nswz](int k) { return k ^ ((k >> 3) & nswz); };
-    // Row stores of the finished tile, 32 bytes per thread: thread -> rows
-    // r0, r0 + NT/(TILE/2), ... of the column pair (pc, pc + 1); the loads of a
-    // batch are issued before its stores.  Column pc keeps ra rows, pc + 1 rb <= ra
-    // (they differ only where y ends inside the pair, ST_C).
-    auto store_pairs = [&](const Out2 &o, int ra, int rb) {
-      constexpr int PR = TILE / 2, RS = NT / PR, NB = 2;
-      const int pc = 2 * (threadIdx.x % PR);
-      if (c0 + pc >= a.L2) return;
-      const cplx *s0 = ex + pc * CS, *s1 = s0 + CS;
-      int r = threadIdx.x / PR;
-      cplx *d = static_cast<cplx *>(o.ptr) + item * o.item_stride + c0 + pc + (long long)r * o.s1;
-      const long long step = (long long)RS * o.s1;
-      for (; r < rb; r += NB * RS, d += NB * step) {
-        cplx u[NB], v2[NB];
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-          if (r + i * RS < rb) {
-            u[i] = s0[nat(r + i * RS)];
-            v2[i] = s1[nat(r + i * RS)];
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < NB; ++i)
-          if (r + i * RS < rb) st256(d + i * step, u[i], v2[i]);
-      }
-      // the rows only column pc has (at most one, where y ends)
-      for (int q = rb + (int)(threadIdx.x / PR); q < ra; q += RS)
-        static_cast<cplx *>(o.ptr)[item * o.item_stride + c0 + pc + (long long)q * o.s1] =
-            s0[nat(q)];
-    };
     constexpr bool TW_A = !PAIR && !SC;
     const cplx tws = TW_A ? tw4(a, (long long)n2 * (L1 / RL)) : make_double2(1.0, 0.0);
 #pragma unroll
@@ -477,6 +452,14 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
           ex[k * TILE + c] = x;  // row-major staging for the TMA store
         else
           col[nat(k)] = x;
+      }
+    }
+    // PAIR: the split's twiddles are requested before the barrier, not after it
+    cplx ps_wk = make_double2(1.0, 0.0), ps_step = ps_wk;
+    if constexpr (PAIR) {
+      if (!g.tma_out) {
+        ps_wk = tw4(a, (long long)n2 * t);
+        ps_step = tw4(a, (long long)n2 * T);
       }
     }
     bar();
@@ -537,8 +520,8 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
       // rows above L1/2 are never stored for the Hermitian product: skip their
       // twiddles and products (3 of the 6 complex multiplies per pair)
       const bool upper = rows_out > L1 / 2 + 1;
-      cplx wk = tw4(a, (long long)n2 * t);
-      const cplx wstep = tw4(a, (long long)n2 * T);
+      cplx wk = ps_wk;
+      const cplx wstep = ps_step;
       const cplx wl1 = upper ? tw4(a, (long long)n2 * L1) : make_double2(1.0, 0.0);
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
@@ -563,12 +546,6 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
       bar();
       // thread -> fixed column cc = tid % TILE, rows r0, r0 + NT/TILE, ...
       auto store_rows = [&](const Out2 &o) {
-        if constexpr (!DEC && TILE % 2 == 0) {
-          if (g.wide_out) {
-            store_pairs(o, rows_out, rows_out);
-            return;
-          }
-        }
         const int cc = DEC ? cg : threadIdx.x % TILE;
         if (c0 + cc >= a.L2) return;
         constexpr int RS = DEC ? T : NT / TILE;
@@ -593,15 +570,8 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
     } else if constexpr (!SC) {
       const Out2 &o = a.out;
       const int rows = o.e1 < L1 ? o.e1 : L1;
-      bool done = false;
-      if constexpr (!DEC && TILE % 2 == 0) {
-        if (g.wide_out) {
-          store_pairs(o, rows, rows);
-          done = true;
-        }
-      }
       const int cc = DEC ? cg : threadIdx.x % TILE;
-      if (!done && c0 + cc < o.e2) {
+      if (c0 + cc < o.e2) {
         constexpr int RS = DEC ? T : NT / TILE;
         const cplx *src = ex + cc * CS;
         int r = DEC ? (int)(threadIdx.x % T) : threadIdx.x / TILE;
@@ -616,16 +586,8 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
         const long long kr = g.c_q + (n2c < g.c_rem ? 1 : 0);
         return (int)(kr < L1 ? kr : L1);
       };
-      bool done = false;
-      if constexpr (!DEC && TILE % 2 == 0) {
-        if (g.wide_out) {
-          const int pc = 2 * (threadIdx.x % (TILE / 2));
-          store_pairs(o, nrows(c0 + pc), nrows(c0 + pc + 1));
-          done = true;
-        }
-      }
       const int cc = DEC ? cg : threadIdx.x % TILE;
-      if (!done && c0 + cc < a.L2) {
+      if (c0 + cc < a.L2) {
         const int rows = nrows(c0 + cc);
         constexpr int RS = DEC ? T : NT / TILE;
         const cplx *src = ex + cc * CS;
@@ -751,14 +713,6 @@ static cudaError_t launch_cols_tma_t(int stage, const ColArgs &a, long long item
     const long long r = std::min<long long>(a.L1, rows + (tail > 0 ? 1 : 0));
     return (int)((r + 255) / 256);
   };
-  // 32-byte row stores (HK_COL_WIDE=1; they need even strides and a 32-byte
-  // aligned base).  Measured on B200 cfg3: 371.6 us against 369.8 us for the
-  // 16-byte stores -- the store path is bound per 32-byte sector, not per
-  // instruction -- so they stay opt-in.
-  auto wide_ok = [&](const Out2 &o) {
-    return TILE % 2 == 0 && L2 % 2 == 0 && o.s2 == 1 && o.s1 % 2 == 0 && o.item_stride % 2 == 0 &&
-           (reinterpret_cast<uintptr_t>(o.ptr) & 31) == 0 && getenv("HK_COL_WIDE");
-  };
   if (stage == ST_A_PAIR) {
     const Op2 &h = a.in, &x = a.in2;
     if (h.kind != FK_F64 || x.kind != FK_F64 || h.s1 != L2 || h.s2 != 1 || x.s1 != L2 ||
@@ -785,7 +739,6 @@ static cudaError_t launch_cols_tma_t(int stage, const ColArgs &a, long long item
     if ((g.fb_in > 0 && !encode4(&g.m_in4, h.ptr, L2, g.fb_in, items, L2, h.item_stride, TILE)) ||
         (g.fb_in2 > 0 && !encode4(&g.m_in24, x.ptr, L2, g.fb_in2, items, L2, x.item_stride, TILE)))
       return cudaErrorNotSupported;
-    g.wide_out = wide_ok(o1) && wide_ok(o2) && o1.e2 == L2 && o2.e2 == L2;
     return launch_t<PL, TILE, ST_A_PAIR>(g, items, ncols, stream);
   }
   if (stage == ST_A_FWD || stage == ST_A_INV) {
@@ -808,7 +761,6 @@ static cudaError_t launch_cols_tma_t(int stage, const ColArgs &a, long long item
     if (g.fb_in > 0 &&
         !encode4(&g.m_in4, op.ptr, f * L2, g.fb_in, items, f * L2, f * op.item_stride, f * TILE))
       return cudaErrorNotSupported;
-    g.wide_out = wide_ok(o) && o.e2 == L2;
     return stage == ST_A_FWD ? launch_t<PL, TILE, ST_A_FWD>(g, items, ncols, stream)
                              : launch_t<PL, TILE, ST_A_INV>(g, items, ncols, stream);
   }
@@ -834,7 +786,6 @@ static cudaError_t launch_cols_tma_t(int stage, const ColArgs &a, long long item
       return cudaErrorNotSupported;
     g.c_q = o.len / L2;
     g.c_rem = o.len - g.c_q * L2;
-    g.wide_out = wide_ok(o) && o.len >= 0;
     return launch_t<PL, TILE, ST_C>(g, items, ncols, stream);
   }
   return cudaErrorNotSupported;
