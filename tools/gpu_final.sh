@@ -16,6 +16,13 @@ cap cfg3_colA k_cols_tma 2 "cfg3 1"
 cap cfg3_rows k_hankel_pp 1 "cfg3 1"
 cap cfg3_colC k_cols_tma 3 "cfg3 1"
 cap cfg4_rows k_rows_pp 1 "cfg4 1"
-cap cfg4_xcols k_cols 1 "cfg4 1"
+cap cfg4_hcols k_cols 3 "cfg4 1"
+cap cfg4_xcols k_cols 4 "cfg4 1"
+cap cfg4_ycols k_cols 5 "cfg4 1"
 cap cfg5_combo k_hankel_fast 4 "cfg5 1"
+python tools/raw_summary.py "cfg2 headline=gpurun_out/f_cfg2_pp_raw.csv" "cfg3 packed column pass=gpurun_out/f_cfg3_colA_raw.csv" \
+  "cfg3 row stage=gpurun_out/f_cfg3_rows_raw.csv" "cfg3 final column pass=gpurun_out/f_cfg3_colC_raw.csv" \
+  "cfg4 h column pass=gpurun_out/f_cfg4_hcols_raw.csv" "cfg4 x column pass=gpurun_out/f_cfg4_xcols_raw.csv" \
+  "cfg4 row stage=gpurun_out/f_cfg4_rows_raw.csv" "cfg4 final column pass=gpurun_out/f_cfg4_ycols_raw.csv" \
+  "cfg5 combo products=gpurun_out/f_cfg5_combo_raw.csv" > gpurun_out/f_summary.txt
 echo done > gpurun_out/f_done
