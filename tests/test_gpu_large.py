@@ -134,3 +134,26 @@ def test_real_pair_column_pass(L1):
         assert strict_relerr(y[b], ref) <= TOL
         a_ref = O.hankel_tvp_full(h[b], shape, [x[b]] * 3)
         assert abs(a[b] - a_ref) <= TOL * abs(a_ref)
+
+
+@pytest.mark.parametrize("shape", [
+    # x rows (n / 4096) below one 256-row block: no 4-D block copy for x, one partial box
+    (7_500_000, 500_000, 500_000),
+    # x rows an exact multiple of 256 (512 rows, no partial row, no partial block)
+    (5_000_000, 1 << 21, 1 << 21),
+    # partial last row inside a partial block for both operands
+    (4_500_000, 2_000_000, 2_000_000),
+])
+def test_packed_real_tma_column_blocks(shape):
+    """Real h and one real vector at L = 3072 x 4096 (packed TMA column pass,
+    Hermitian half): operand row counts around the 256-row block edges of the
+    4-D / 3-D tensor copies (reference hankel.py:140-147, padded oracle)."""
+    rng = np.random.default_rng(shape[1] % 1000)
+    d = sum(shape) - 2
+    assert (1 << 23) < d <= 3 * (1 << 22)
+    h = rng.standard_normal(d)
+    x = rng.uniform(-1.0, 1.0, shape[1])
+    y = batched.hankel_tvp_partial(torch.from_numpy(h).cuda()[None],
+                                   [torch.from_numpy(x).cuda()[None]] * 2, shape)[0].cpu().numpy()
+    ref = O.hankel_tvp_partial_padded(h, shape, [x, x], length=1 << 24)
+    assert strict_relerr(y, ref) <= TOL
