@@ -122,6 +122,17 @@ __device__ __forceinline__ cplx tw4(const ColArgs &a, long long e) {
   return cmul(__ldg(&a.thi[e >> 12]), __ldg(&a.tlo[e & 4095]));
 }
 
+// The two table reads of a W_L^e lookup without their product: issued ahead of
+// a wait or barrier, multiplied after it (the loads then overlap the wait).
+struct Tw4Raw {
+  cplx hi, lo;
+  __device__ __forceinline__ cplx get() const { return cmul(hi, lo); }
+};
+__device__ __forceinline__ Tw4Raw tw4_raw(const ColArgs &a, long long e) {
+  if (e >= a.L) e -= a.L;
+  return Tw4Raw{__ldg(&a.thi[e >> 12]), __ldg(&a.tlo[e & 4095])};
+}
+
 // Column-pass twiddles in TMEM (r02): a thread's twiddles are the same for
 // every tile (pass 0: W_L1^{j beta} of its NB0 butterflies, pass 1: W_256^{j lo}),
 // so they are read once from the W_L1 table and kept next to nothing else in
@@ -294,20 +305,24 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
     // reads that miss L1 next to 197 KB of shared memory) are requested before
     // the wait for the tile, not between the wait and the first butterfly
     constexpr int NB0 = ColTw<PL>::NB0;
-    cplx pz_step = make_double2(1.0, 0.0), pz_row = pz_step, pz_cur[NB0];
+    const Tw4Raw one_raw{make_double2(1.0, 0.0), make_double2(1.0, 0.0)};
+    Tw4Raw rz_step = one_raw, rz_row = one_raw, rz_cur[NB0];
     if constexpr (SC) {
       const int c = DEC ? cg : threadIdx.x % TILE;
       const int tp = DEC ? (int)(threadIdx.x % T) : threadIdx.x / TILE;
       const int n2 = c0 + c;
-      pz_step = tw4(a, (long long)n2 * PL::stride(0));
-      if (a.half) pz_row = tw4(a, (long long)n2 * L1);  // W_L2^{n2}
+      rz_step = tw4_raw(a, (long long)n2 * PL::stride(0));
+      if (a.half) rz_row = tw4_raw(a, (long long)n2 * L1);  // W_L2^{n2}
 #pragma unroll
       for (int i = 0; i < NB0; ++i) {
         const int beta = tp + i * T;
-        pz_cur[i] = beta < L1 / R0 ? tw4(a, (long long)n2 * beta) : pz_step;
+        rz_cur[i] = beta < L1 / R0 ? tw4_raw(a, (long long)n2 * beta) : rz_step;
       }
     }
     tma::mbar_wait(mb, (uint32_t)(it & 1));
+    cplx pz_step = rz_step.get(), pz_row = rz_row.get(), pz_cur[NB0];
+#pragma unroll
+    for (int i = 0; i < NB0; ++i) pz_cur[i] = rz_cur[i].get();
     if (g.tma_out) {  // the previous tile's TMA stores have read the exchange buffer
       if (threadIdx.x == 0) tma::bulk_wait_read();
       if constexpr (SC) __syncthreads();
@@ -455,14 +470,15 @@ __global__ void __launch_bounds__(TILE * PL::T, 1)
       }
     }
     // PAIR: the split's twiddles are requested before the barrier, not after it
-    cplx ps_wk = make_double2(1.0, 0.0), ps_step = ps_wk;
+    Tw4Raw rs_wk = one_raw, rs_step = one_raw;
     if constexpr (PAIR) {
       if (!g.tma_out) {
-        ps_wk = tw4(a, (long long)n2 * t);
-        ps_step = tw4(a, (long long)n2 * T);
+        rs_wk = tw4_raw(a, (long long)n2 * t);
+        rs_step = tw4_raw(a, (long long)n2 * T);
       }
     }
     bar();
+    const cplx ps_wk = rs_wk.get(), ps_step = rs_step.get();
     if (g.tma_out) {
       // ---- TMA-store epilogue
       if constexpr (PAIR) {
