@@ -106,6 +106,22 @@ __global__ void __launch_bounds__(TILE * PL::T, (col_blocks<PL, TILE>())) k_cols
   const Lim lim_out = make_lim(a.out.len, a.out.e1, a.out.e2);
   const Lim lim_out2 = PAIR ? make_lim(a.out2.len, a.out2.e1, a.out2.e2) : Lim{0, 0, 0};
 
+  // Pruned first / last passes (the 2D block product's vector and output
+  // passes, cfg4: 64 of 192 rows).  First pass: rows >= NZP * stride(0) of the
+  // operand are zero, so each pass-0 butterfly has NZP nonzero inputs and the
+  // zero rows are neither copied nor read.  Last pass: only rows < NOP * L1/RL
+  // of the output are kept (register j of a last-pass butterfly holds row
+  // k0 + j L1/RL), so NOP of the RL outputs are computed and stored.
+  constexpr int NZP0 = PL::P > 1 ? (R0 % 3 == 0 ? R0 / 3 : R0 / 4) : R0;
+  constexpr int NZP = NZP0 < 1 ? R0 : NZP0;  // radix 2 first passes are not pruned
+  constexpr int NOP = (PL::P > 1 && RL == 16) ? 6 : RL;
+  constexpr int S0K = PL::stride(0);
+  const int in_rows = lim_in.q + (lim_in.rem > 0 ? 1 : 0);    // max rows of any column
+  const int out_rows = lim_out.q + (lim_out.rem > 0 ? 1 : 0);
+  const bool prune_in = !PAIR && STAGE != ST_C && NZP < R0 && in_rows <= NZP * S0K;
+  const bool prune_out = STAGE == ST_C && NOP < RL && out_rows <= NOP * (L1 / RL);
+  const int need_rows = prune_in ? NZP * S0K : L1;  // tile rows the first pass reads
+
   // Tile load.  r02 ncu (cfg4 h pass): the per-element index arithmetic of the
   // generic loop (runtime divisions, 64-bit bounds and three 64-bit multiplies
   // per element, ~40 integer instructions) was 35% of the kernel.  Here the
@@ -134,6 +150,7 @@ __global__ void __launch_bounds__(TILE * PL::T, (col_blocks<PL, TILE>())) k_cols
     const char *b2 = PAIR ? static_cast<const char *>(a.in2.ptr) + item * a.in2.item_stride * 8
                           : nullptr;
     auto one = [&](int cc, int n1d, int rows, int rows2) {
+      if (n1d >= need_rows) return;  // pruned first pass: zero rows are never read
       // Hermitian half (ST_C): rows above L1/2 are read from row L1 - n1
       const int n1 = (half_c && 2 * n1d > L1) ? L1 - n1d : n1d;
       const uint32_t n2 = (uint32_t)(c0 + cc);
@@ -235,7 +252,10 @@ __global__ void __launch_bounds__(TILE * PL::T, (col_blocks<PL, TILE>())) k_cols
     cplx v[V];
     auto r_store = [&](int i, int j, int, cplx x) { v[i * RL + j] = x; };
     if constexpr (PL::P > 1) {
-      fast::pass<PL, 0, INV, false, R0, R0>(t, a.ctw, tw0, in_load, s_store);
+      if (NZP < R0 && prune_in)
+        fast::pass<PL, 0, INV, false, NZP, R0>(t, a.ctw, tw0, in_load, s_store);
+      else
+        fast::pass<PL, 0, INV, false, R0, R0>(t, a.ctw, tw0, in_load, s_store);
       sfor<PL::P - 2>([&](auto qc) {
         constexpr int q = decltype(qc)::value + 1;
         __syncthreads();
@@ -243,7 +263,10 @@ __global__ void __launch_bounds__(TILE * PL::T, (col_blocks<PL, TILE>())) k_cols
                                                                  s_store);
       });
       __syncthreads();
-      fast::pass<PL, PL::P - 1, INV, false, RL, RL, L1, kColRec>(t, a.ctw, tw0, s_load, r_store);
+      if (prune_out)
+        fast::pass<PL, PL::P - 1, INV, false, RL, NOP, L1, kColRec>(t, a.ctw, tw0, s_load, r_store);
+      else
+        fast::pass<PL, PL::P - 1, INV, false, RL, RL, L1, kColRec>(t, a.ctw, tw0, s_load, r_store);
     } else {
       fast::pass<PL, 0, INV, false, R0, R0>(t, a.ctw, tw0, in_load, r_store);
     }
@@ -268,6 +291,7 @@ __global__ void __launch_bounds__(TILE * PL::T, (col_blocks<PL, TILE>())) k_cols
                                      : make_double2(1.0, 0.0);
 #pragma unroll
       for (int j = 0; j < RL; ++j) {
+        if (prune_out && j >= NOP) break;
         const int k = k0 + j * (L1 / RL);
         cplx x = v[i * RL + j];
         if (TW_A && a.twiddle) {
