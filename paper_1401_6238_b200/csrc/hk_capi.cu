@@ -494,8 +494,9 @@ int hk_plan_create_block(hk_plan **plan, int order, int levels, const int64_t *l
     // rows run on the all-radix-16 plans (256, 4096: immediate-offset smem
     // addressing) when that costs at most 40% more length, e.g. 190 -> 256
     // rather than 192: measured faster on B200 despite the extra points
+    // HK_PP192=1 (A/B): keep 192-point rows for the 16 x 12 ping-pong row kernel
     for (long long l2 : {256LL, 4096LL})
-      if (l2 >= din && l2 != L2 && l2 * 10 <= L2 * 14) {
+      if (l2 >= din && l2 != L2 && l2 * 10 <= L2 * 14 && !(L2 == 192 && getenv("HK_PP192"))) {
         L2 = l2;
         break;
       }

@@ -235,10 +235,17 @@ __device__ __forceinline__ void pass(int t, const C *__restrict__ tw, const TW0 
       }
     }
   }
+  // Fewer butterflies than threads inside one warp (192 = 16 x 12 on 16
+  // threads): the idle threads run butterfly 0 with their stores masked
+  // instead of branching around it, because the TMEM twiddle reads inside are
+  // warp-collective (tcgen05.ld.sync.aligned).
+  constexpr bool kPred = NBUT < PL::T && PL::T <= 32;
 #pragma unroll
   for (int i = 0; i < NB; ++i) {
-    const int beta = t + i * PL::T;
-    if (NBUT % PL::T == 0 || beta < NBUT) {
+    const int beta_raw = t + i * PL::T;
+    const bool live = NBUT % PL::T == 0 || beta_raw < NBUT;
+    const int beta = (kPred && !live) ? 0 : beta_raw;
+    if (kPred || live) {
       int lo, hi;
       if constexpr (HIM) {
         hi = beta % H;
@@ -336,6 +343,7 @@ __device__ __forceinline__ void pass(int t, const C *__restrict__ tw, const TW0 
         twiddle();
       }
       pre_store();
+      if (kPred && !live) continue;
       if constexpr (std::is_same_v<std::decay_t<Store>, SmemIO>) {
         const HexAddr<Q> ad(store.sbase, base);
         sfor<NOUT>([&](auto jc) {

@@ -550,7 +550,17 @@ __global__ void __launch_bounds__(512, 1) k_rows_pp(const __grid_constant__ Args
 #pragma unroll
     for (int c = 0; c < (R0 - 1 + 3) / 4; ++c) {
       cplx w[4];
-      g0.chunk(t, c, w);
+      if constexpr (L == 256) {
+        g0.chunk(t, c, w);
+      } else {
+        // plans without a thread-major first-pass table (192 = 16 x 12): W_L^{j t}
+        // straight from the W_L table, once per CTA
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = 4 * c + q + 1;
+          w[q] = (j < R0 && t < L / R0) ? a.tw[(j * t) % L] : make_double2(1.0, 0.0);
+        }
+      }
       tmem_st4(ttw + 16 * c, w);
     }
     tmem_wait_st();
@@ -726,11 +736,30 @@ static cudaError_t launch_pp_256(const Args1D &a, cudaStream_t stream) {
   return pp::launch_rows_pp<PL, 4, 16, 16, 8>(a, stream);
 }
 
+// 192-point batched rows (2D block row stage at the exact padded length
+// 192 >= d_in = 190 instead of 256): 16 threads per product as for 256, 12
+// values per thread, radix 16 then radix 12 (12 of the 16 threads run the
+// radix-16 pass; every thread one radix-12 butterfly).
+static cudaError_t launch_pp_192(const Args1D &a, cudaStream_t stream) {
+  if (a.mode != M_PARTIAL || a.nfac != 1 || !a.tw || a.nsub < 1 || a.ncombo)
+    return cudaErrorNotSupported;
+  const Factor &h = a.h, &x = a.fac[0];
+  if (h.kind != FK_C128 || x.kind != FK_C128 || h.estride != 1 || x.estride != 1 ||
+      a.out_estride != 1 || h.len > 192 || h.len <= 0 || x.len <= 0 || x.len > 72 ||
+      a.out_len > 72)
+    return cudaErrorNotSupported;
+  if ((reinterpret_cast<uintptr_t>(h.ptr) | reinterpret_cast<uintptr_t>(x.ptr)) & 15)
+    return cudaErrorNotSupported;
+  using PL = Plan1D<192, 16, 16, 12>;
+  return pp::launch_rows_pp<PL, 6, 6, 16, 8>(a, stream);
+}
+
 // Ping-pong TMA path; cudaErrorNotSupported unless the request is the plain
 // batched H x^{m-1} shape it implements.
 cudaError_t launch_pp_1d(int L, const Args1D &a, cudaStream_t stream) {
   if (getenv("HK_NO_PP")) return cudaErrorNotSupported;
   if (L == 256) return launch_pp_256(a, stream);
+  if (L == 192 && getenv("HK_PP192")) return launch_pp_192(a, stream);
   if (L != 4096 || a.mode != M_PARTIAL || a.nfac != 1 || !a.tw0 || a.nsub < 1 || a.ncombo)
     return cudaErrorNotSupported;
   const Factor &h = a.h, &x = a.fac[0];
