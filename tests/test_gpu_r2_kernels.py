@@ -138,3 +138,25 @@ def test_block_rows_pp256_vs_fast_rows(monkeypatch, block, outer, B):
         xv = X[b].reshape(-1)
         ref = O.bhhb_tvp_partial(H[b], block, outer, [xv] * (m - 1))
         assert strict_relerr(y[b], ref) <= TOL
+
+
+@pytest.mark.parametrize("block,outer,B", [((62, 62, 62), (28, 28, 28), 3),
+                                           ((64, 64, 64), (63, 63, 63), 2)])
+def test_block_rows_pp192_opt_in(monkeypatch, block, outer, B):
+    """HK_PP192=1 (read when the plan is created: shapes no other test uses):
+    the row stage at the exact padded length 192 = 16 x 12 on the ping-pong row
+    kernel, 16 threads per product with 12 live in the radix-16 pass, against
+    the oracle (reference block.py:136-144)."""
+    monkeypatch.setenv("HK_PP192", "1")
+    rng = np.random.default_rng(sum(block) + 7 * sum(outer) + B)
+    m = len(block)
+    din, dout = sum(block) - m + 1, sum(outer) - m + 1
+    assert 128 < din <= 192
+    H = rand_vec(rng, B * din * dout).reshape(B, din, dout)
+    X = rand_vec(rng, B * block[1] * outer[1]).reshape(B, outer[1], block[1])  # (B, N, n)
+    dH = torch.from_numpy(H).cuda()
+    dx = torch.from_numpy(np.ascontiguousarray(X)).cuda().reshape(B, -1)
+    y = batched.bhhb_tvp_partial(dH, [dx] * (m - 1), m, block, outer).cpu().numpy()
+    for b in range(B):
+        ref = O.bhhb_tvp_partial(H[b], block, outer, [X[b].reshape(-1)] * (m - 1))
+        assert strict_relerr(y[b], ref) <= TOL
