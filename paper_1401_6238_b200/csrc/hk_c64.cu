@@ -395,11 +395,218 @@ static cudaError_t launch_c64_plan(const Args1D &a, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Ping-pong variant for the batched H x^{m-1} workload in complex64 (cfg2-c64):
+// the structure of the complex128 headline kernel (hk_pp1d.cu) on float2.  One
+// 512-thread CTA per SM runs two 256-thread product groups; each group stages
+// the operands of its product after next with per-thread 8-byte cp.async into
+// its OWN h and x staging buffers (odd-length complex64 rows are only 8-byte
+// aligned, so the 16-byte bulk copies of the complex128 kernel do not apply)
+// right after the first pass has consumed them, so global latency is a full
+// product period off the critical path.  The spectral accumulator and the
+// per-thread twiddles of both twiddled passes live in TMEM; pass 1 runs
+// lo-major so the pass-1/pass-2 exchanges stay inside each warp.
+//   smem: ex[2][L] | hs[2][L] | xs[2][XS]   (float2; 147 KB at L = 4096)
+//   TMEM: cols [0,128) accumulators (32 per warp slab) | [128,192) pass-0
+//         twiddles | [192,256) pass-1 twiddles (slabs shared by the two groups)
+namespace ppf {
+
+template <int N>
+struct GroupBar {
+  int id;
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "n"(N) : "memory");
+  }
+};
+
+struct Tw01F {
+  uint32_t taddr0, taddr1;
+  __device__ __forceinline__ void chunk(int, int c, cplxf *w) const { tmem_ld4f(taddr0 + 8 * c, w); }
+  __device__ __forceinline__ void chunk1(int c, cplxf *w) const { tmem_ld4f(taddr1 + 8 * c, w); }
+};
+
+template <class PL, int NZ, int NO>
+__global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp_c64(const __grid_constant__ Args1D a) {
+  constexpr int L = PL::L, T = PL::T, V = PL::V, R0 = PL::radix[0], R1 = PL::radix[1];
+  constexpr int S0 = PL::stride(0), XS = NZ * S0, TW1 = L / R0;
+  static_assert(PL::G == 1 && T == 256 && PL::P == 3 && L / R0 == T && NZ < R0,
+                "one product per 256-thread group, three passes, staged x prefix");
+  static_assert(R1 == PL::Rlast && 32 % PL::Rlast == 0, "warp-local last exchange");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint32_t tmem_slot;
+  cplxf *ex = reinterpret_cast<cplxf *>(smem_raw);
+  cplxf *hs = ex + 2 * L;
+  cplxf *xs = hs + 2 * L;
+  const int warp = threadIdx.x >> 5;
+  const int g = threadIdx.x / T, t = threadIdx.x - g * T;
+  // positions the copies never write: zero once (the padding of h~ and x~)
+  for (int i = threadIdx.x; i < 2 * L; i += blockDim.x)
+    if (i % L >= a.h.len) hs[i] = make_float2(0.f, 0.f);
+  for (int i = threadIdx.x; i < 2 * XS; i += blockDim.x)
+    if (i % XS >= a.fac[0].len) xs[i] = make_float2(0.f, 0.f);
+  if (warp == 0) tmem_alloc<256>(&tmem_slot);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t lane_q = (uint32_t)(32 * (warp & 3)) << 16;
+  const uint32_t tacc = tmem_slot + lane_q + (uint32_t)((warp >> 2) * 32);
+  const uint32_t ttw = tmem_slot + lane_q + 128u + (uint32_t)(((warp >> 2) & 1) * 32);
+  const uint32_t ttw1 = ttw + 64u;
+  if (g == 0) {  // a thread's twiddles depend only on its index in its group
+    const int lo1 = t % PL::stride(1);
+#pragma unroll
+    for (int c = 0; c < (R0 - 1 + 3) / 4; ++c) {
+      cplxf w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = 4 * c + q + 1;
+        w[q] = j < R0 ? a.twf[(j * t) % L] : make_float2(1.f, 0.f);  // W_L^{j t}
+      }
+      tmem_st4f(ttw + 8 * c, w);
+    }
+#pragma unroll
+    for (int c = 0; c < (R1 - 1 + 3) / 4; ++c) {
+      cplxf w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = 4 * c + q + 1;  // W_{L/R0}^{j lo} = W_L^{R0 j lo}
+        w[q] = j < R1 ? a.twf[((j * lo1) % TW1) * R0] : make_float2(1.f, 0.f);
+      }
+      tmem_st4f(ttw1 + 8 * c, w);
+    }
+    tmem_wait_st();
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const Tw01F tw0{ttw, ttw1};
+
+  const long long nloc =
+      a.batch > blockIdx.x ? (a.batch - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  cplxf *sbuf = ex + g * L, *my_h = hs + g * L, *my_x = xs + g * XS;
+  const uint32_t sh = smem_u32(my_h), sx = smem_u32(my_x);
+  auto issue_h = [&](long long k) {
+    const cplxf *src = static_cast<const cplxf *>(a.h.ptr) +
+                       (blockIdx.x + k * (long long)gridDim.x) * a.h.bstride;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int pos = t + i * T;
+      if (pos < a.h.len) fast::cpa8(sh + 8u * pos, src + pos, true);
+    }
+  };
+  auto issue_x = [&](long long k) {
+    const cplxf *src = static_cast<const cplxf *>(a.fac[0].ptr) +
+                       (blockIdx.x + k * (long long)gridDim.x) * a.fac[0].bstride;
+#pragma unroll
+    for (int i = 0; i < NZ; ++i) {
+      const int pos = t + i * T;
+      if (pos < a.fac[0].len) fast::cpa8(sx + 8u * pos, src + pos, true);
+    }
+  };
+  const GroupBar<T> sync{1 + g};
+  if (g < nloc) {
+    issue_h(g);
+    issue_x(g);
+  }
+  const float sc = (float)a.scale;
+  for (long long k = g; k < nloc; k += 2) {
+    fast::cpa_wait_all();  // this thread's copies of product k; the entry barrier covers the group
+    cplxf v[V];
+    fast::fft_dif<PL, true, R0, L, false>(
+        sbuf, t, a.twf, tw0, [&](int pos) { return my_h[pos]; }, v, sync,
+        [&]() {
+          if (k + 2 < nloc) issue_h(k + 2);
+        },
+        (fast::WarpSync *)nullptr);
+    tmem_wait_st();
+#pragma unroll
+    for (int c = 0; c < V / 4; ++c) tmem_st4f(tacc + 8 * c, &v[4 * c]);
+    fast::fft_dif<PL, false, NZ, L, false>(
+        sbuf, t, a.twf, tw0, [&](int pos) { return my_x[pos]; }, v, sync,
+        [&]() {
+          if (k + 2 < nloc) issue_x(k + 2);
+        },
+        (fast::WarpSync *)nullptr);
+    tmem_wait_st();
+#pragma unroll
+    for (int c = 0; c < V / 4; ++c) {
+      cplxf acc[4];
+      tmem_ld4f(tacc + 8 * c, acc);
+      for (int q = 0; q < a.fac[0].power; ++q) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[e] = cmul(acc[e], v[4 * c + e]);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[4 * c + e] = acc[e];
+    }
+    cplxf *yk = static_cast<cplxf *>(a.out) +
+                (blockIdx.x + k * (long long)gridDim.x) * a.out_bstride;
+    fast::fft_final<PL, NO, L, false>(
+        sbuf, t, a.twf, tw0, v,
+        [&](int pos, cplxf val) {
+          if (pos < a.out_len) yk[pos] = make_float2(val.x * sc, val.y * sc);
+        },
+        sync, (fast::WarpSync *)nullptr);
+  }
+  fast::cpa_wait_all();
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tmem_fence_after();
+    tmem_dealloc<256>(tmem_slot);
+  }
+}
+
+template <class PL, int NZ, int NO>
+static cudaError_t launch(const Args1D &a, cudaStream_t stream) {
+  const int smem = (4 * PL::L + 2 * NZ * PL::stride(0)) * (int)sizeof(cplxf) + 128;
+  static std::atomic<unsigned long long> configured{0};
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(configured.load() & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(k_hankel_pp_c64<PL, NZ, NO>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+    configured.fetch_or(bit);
+  }
+  long long grid = sms[dev & 63];
+  if (grid > a.batch) grid = a.batch;
+  if (grid <= 0) return cudaSuccess;
+  k_hankel_pp_c64<PL, NZ, NO><<<(unsigned)grid, 2 * PL::T, smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace ppf
+
+// cudaErrorNotSupported unless the request is the plain batched complex64
+// H x^{m-1} shape of the ping-pong kernel (HK_NO_PP_C64=1 turns it off for A/B).
+static cudaError_t launch_pp_c64(int L, const Args1D &a, cudaStream_t stream) {
+  if (getenv("HK_NO_PP_C64")) return cudaErrorNotSupported;
+  if (L != 4096 || a.mode != M_PARTIAL || a.nfac != 1 || a.nsub != 1 || a.ncombo)
+    return cudaErrorNotSupported;
+  const Factor &h = a.h, &x = a.fac[0];
+  if (h.kind != FK_C64 || x.kind != FK_C64 || h.estride != 1 || x.estride != 1 ||
+      a.out_estride != 1 || h.len <= 0 || h.len > L || x.len <= 0)
+    return cudaErrorNotSupported;
+  if ((reinterpret_cast<uintptr_t>(h.ptr) | reinterpret_cast<uintptr_t>(x.ptr)) & 7)
+    return cudaErrorNotSupported;
+  using PL = Plan1D<4096, 256, 16, 16, 16>;
+  constexpr int s0 = PL::stride(0);
+  const int nz = (x.len + s0 - 1) / s0, no = (a.out_len + s0 - 1) / s0;
+  if (nz <= 4 && no <= 4) return ppf::launch<PL, 4, 4>(a, stream);
+  return cudaErrorNotSupported;
+}
+
 cudaError_t launch_c64_1d(int L, const Args1D &a, cudaStream_t stream) {
   if (!a.twf) return cudaErrorInvalidValue;
   if (a.mode != M_PARTIAL && a.mode != M_FULL) return cudaErrorNotSupported;
   static const bool generic_only = getenv("HK_C64_GENERIC") != nullptr;  // A/B switch
   if (!generic_only) {
+    const cudaError_t e = launch_pp_c64(L, a, stream);
+    if (e != cudaErrorNotSupported) return e;
     int maxlen = 1;
     for (int f = 0; f < a.nfac; ++f)
       if (a.fac[f].len > maxlen) maxlen = a.fac[f].len;
