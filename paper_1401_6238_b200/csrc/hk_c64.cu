@@ -425,32 +425,33 @@ struct Tw01F {
   __device__ __forceinline__ void chunk1(int c, cplxf *w) const { tmem_ld4f(taddr1 + 8 * c, w); }
 };
 
-template <class PL, int NZ, int NO>
-__global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp_c64(const __grid_constant__ Args1D a) {
+template <class PL, int NZ, int NO, int NG>
+__global__ void __launch_bounds__(NG * PL::T, 1) k_hankel_pp_c64(const __grid_constant__ Args1D a) {
   constexpr int L = PL::L, T = PL::T, V = PL::V, R0 = PL::radix[0], R1 = PL::radix[1];
   constexpr int S0 = PL::stride(0), XS = NZ * S0, TW1 = L / R0;
+  constexpr int TC = NG * 64 + 128 <= 256 ? 256 : 512;  // accumulators + two twiddle slabs
   static_assert(PL::G == 1 && T == 256 && PL::P == 3 && L / R0 == T && NZ < R0,
                 "one product per 256-thread group, three passes, staged x prefix");
   static_assert(R1 == PL::Rlast && 32 % PL::Rlast == 0, "warp-local last exchange");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
   cplxf *ex = reinterpret_cast<cplxf *>(smem_raw);
-  cplxf *hs = ex + 2 * L;
-  cplxf *xs = hs + 2 * L;
+  cplxf *hs = ex + NG * L;
+  cplxf *xs = hs + NG * L;
   const int warp = threadIdx.x >> 5;
   const int g = threadIdx.x / T, t = threadIdx.x - g * T;
   // positions the copies never write: zero once (the padding of h~ and x~)
-  for (int i = threadIdx.x; i < 2 * L; i += blockDim.x)
+  for (int i = threadIdx.x; i < NG * L; i += blockDim.x)
     if (i % L >= a.h.len) hs[i] = make_float2(0.f, 0.f);
-  for (int i = threadIdx.x; i < 2 * XS; i += blockDim.x)
+  for (int i = threadIdx.x; i < NG * XS; i += blockDim.x)
     if (i % XS >= a.fac[0].len) xs[i] = make_float2(0.f, 0.f);
-  if (warp == 0) tmem_alloc<256>(&tmem_slot);
+  if (warp == 0) tmem_alloc<TC>(&tmem_slot);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
   const uint32_t lane_q = (uint32_t)(32 * (warp & 3)) << 16;
   const uint32_t tacc = tmem_slot + lane_q + (uint32_t)((warp >> 2) * 32);
-  const uint32_t ttw = tmem_slot + lane_q + 128u + (uint32_t)(((warp >> 2) & 1) * 32);
+  const uint32_t ttw = tmem_slot + lane_q + (uint32_t)(NG * 64) + (uint32_t)(((warp >> 2) & 1) * 32);
   const uint32_t ttw1 = ttw + 64u;
   if (g == 0) {  // a thread's twiddles depend only on its index in its group
     const int lo1 = t % PL::stride(1);
@@ -509,13 +510,13 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp_c64(const __grid_con
     issue_x(g);
   }
   const float sc = (float)a.scale;
-  for (long long k = g; k < nloc; k += 2) {
+  for (long long k = g; k < nloc; k += NG) {
     fast::cpa_wait_all();  // this thread's copies of product k; the entry barrier covers the group
     cplxf v[V];
     fast::fft_dif<PL, true, R0, L, false>(
         sbuf, t, a.twf, tw0, [&](int pos) { return my_h[pos]; }, v, sync,
         [&]() {
-          if (k + 2 < nloc) issue_h(k + 2);
+          if (k + NG < nloc) issue_h(k + NG);
         },
         (fast::WarpSync *)nullptr);
     tmem_wait_st();
@@ -524,7 +525,7 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp_c64(const __grid_con
     fast::fft_dif<PL, false, NZ, L, false>(
         sbuf, t, a.twf, tw0, [&](int pos) { return my_x[pos]; }, v, sync,
         [&]() {
-          if (k + 2 < nloc) issue_x(k + 2);
+          if (k + NG < nloc) issue_x(k + NG);
         },
         (fast::WarpSync *)nullptr);
     tmem_wait_st();
@@ -553,20 +554,20 @@ __global__ void __launch_bounds__(2 * PL::T, 1) k_hankel_pp_c64(const __grid_con
   __syncthreads();
   if (warp == 0) {
     tmem_fence_after();
-    tmem_dealloc<256>(tmem_slot);
+    tmem_dealloc<TC>(tmem_slot);
   }
 }
 
-template <class PL, int NZ, int NO>
+template <class PL, int NZ, int NO, int NG>
 static cudaError_t launch(const Args1D &a, cudaStream_t stream) {
-  const int smem = (4 * PL::L + 2 * NZ * PL::stride(0)) * (int)sizeof(cplxf) + 128;
+  const int smem = NG * (2 * PL::L + NZ * PL::stride(0)) * (int)sizeof(cplxf) + 128;
   static std::atomic<unsigned long long> configured{0};
   static int sms[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(configured.load() & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(k_hankel_pp_c64<PL, NZ, NO>,
+    cudaError_t e = cudaFuncSetAttribute(k_hankel_pp_c64<PL, NZ, NO, NG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
@@ -575,7 +576,7 @@ static cudaError_t launch(const Args1D &a, cudaStream_t stream) {
   long long grid = sms[dev & 63];
   if (grid > a.batch) grid = a.batch;
   if (grid <= 0) return cudaSuccess;
-  k_hankel_pp_c64<PL, NZ, NO><<<(unsigned)grid, 2 * PL::T, smem, stream>>>(a);
+  k_hankel_pp_c64<PL, NZ, NO, NG><<<(unsigned)grid, NG * PL::T, smem, stream>>>(a);
   return cudaGetLastError();
 }
 
@@ -596,7 +597,11 @@ static cudaError_t launch_pp_c64(int L, const Args1D &a, cudaStream_t stream) {
   using PL = Plan1D<4096, 256, 16, 16, 16>;
   constexpr int s0 = PL::stride(0);
   const int nz = (x.len + s0 - 1) / s0, no = (a.out_len + s0 - 1) / s0;
-  if (nz <= 4 && no <= 4) return ppf::launch<PL, 4, 4>(a, stream);
+  // three product groups per SM (768 threads, 85 registers) against two (128
+  // registers): HK_PP_C64_NG selects for A/B
+  const int ng = getenv("HK_PP_C64_NG") ? atoi(getenv("HK_PP_C64_NG")) : 2;
+  if (nz <= 4 && no <= 4)
+    return ng == 3 ? ppf::launch<PL, 4, 4, 3>(a, stream) : ppf::launch<PL, 4, 4, 2>(a, stream);
   return cudaErrorNotSupported;
 }
 

@@ -54,17 +54,61 @@ __device__ __forceinline__ cplx cmulc(cplx a, cplx b) {
   return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
 }
 __device__ __forceinline__ cplx cscale(cplx a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ cplx cswapfma(cplx a, double kx, double ky) {
+  return make_double2(fma(kx, a.y, a.x), fma(ky, a.x, a.y));
+}
+__device__ __forceinline__ cplx caxpy(cplx a, double s, cplx b) {
+  return make_double2(fma(s, b.x, a.x), fma(s, b.y, a.y));
+}
 // a * (-i) and a * (+i)
 __device__ __forceinline__ cplx mul_mi(cplx a) { return make_double2(a.y, -a.x); }
 __device__ __forceinline__ cplx mul_pi(cplx a) { return make_double2(-a.y, a.x); }
 
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// complex64: the two components of a float2 sit in an aligned register pair,
+// so sums, differences and real-scalar FMAs are ONE packed sm_100 instruction
+// (FADD2 / FFMA2 on .f32x2) instead of two: the complex64 kernels are bound by
+// instruction issue (FP32 runs at one warp instruction per clock per
+// scheduler), so halving the additive instructions is what speeds them up.
+__device__ __forceinline__ unsigned long long pk2(float2 a) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(unsigned long long r) {
+  float2 c;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(c.x), "=f"(c.y) : "l"(r));
+  return c;
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(r);
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(r);
+}
+// a + s * b, s a real scalar (both components): one FFMA2
+__device__ __forceinline__ float2 caxpy(float2 a, float s, float2 b) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(make_float2(s, s))), "l"(pk2(b)), "l"(pk2(a)));
+  return upk2(r);
+}
+__device__ __forceinline__ unsigned long long pk2s(float x, float y) { return pk2(make_float2(x, y)); }
+// Complex products stay scalar (two FMUL + two FFMA): the packed form needs a
+// (-1, 1) sign pair per product and measured more instructions, not fewer.
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+// a + (kx, ky) .* (a.y, a.x): the (1 + i k) rotations of the radix-16 codelet, one FFMA2
+__device__ __forceinline__ float2 cswapfma(float2 a, float kx, float ky) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2s(kx, ky)), "l"(pk2s(a.y, a.x)), "l"(pk2(a)));
+  return upk2(r);
 }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 __device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }
@@ -309,10 +353,13 @@ __device__ __forceinline__ C tw_u(C b) {
   if constexpr (r == 0) {
     u = b;
   } else if constexpr (r == 2) {  // (1 + i sg)
-    u = sg > 0 ? CT<C>::make(b.x - b.y, b.y + b.x) : CT<C>::make(b.x + b.y, b.y - b.x);
+    if constexpr (sizeof(S) == 4)
+      u = cswapfma(b, (S)-sg, (S)sg);
+    else
+      u = sg > 0 ? CT<C>::make(b.x - b.y, b.y + b.x) : CT<C>::make(b.x + b.y, b.y - b.x);
   } else {  // (1 + i k tau), k = sg * r
     constexpr S kt = (S)(sg * r * kTau);
-    u = CT<C>::make(fma(-kt, b.y, b.x), fma(kt, b.x, b.y));
+    u = cswapfma(b, -kt, kt);
   }
   return rot_i<sg * m>(u);
 }
@@ -325,7 +372,7 @@ __device__ __forceinline__ C axpy(C a, C b) {
     return SIGN > 0 ? cadd(a, b) : csub(a, b);
   } else {
     constexpr S s = (S)(SIGN * sigma_val(CODE));
-    return CT<C>::make(fma(s, b.x, a.x), fma(s, b.y, a.y));
+    return caxpy(a, s, b);
   }
 }
 }  // namespace r16
@@ -369,7 +416,7 @@ __device__ __forceinline__ C cfma_dir(C q, C x, C w) {
 template <class C>
 __device__ __forceinline__ C twice_minus(C q, C s) {
   using S = typename CT<C>::S;
-  return CT<C>::make(fma((S)2, q.x, -s.x), fma((S)2, q.y, -s.y));
+  return CT<C>::make(fma((S)2, q.x, -s.x), fma((S)2, q.y, -s.y));  // (negated addend: scalar form)
 }
 
 // Radix-16 with input twiddles v[j] *= w_j (j = 1..15) folded into the first
