@@ -10,7 +10,12 @@
 // The reference itself is complex128-only (core.py:21-22); this is the
 // batched-API extension SURVEY §7 step 8 / §8(b) list as HK_C64 / HK_F32.
 //
-// Design: half the bytes of a complex128 working set, so the accumulator and
+// Three kernels: the generic and fast kernels below (several products per SM,
+// latency hidden by occupancy) and, for the batched L = 4096 headline shape,
+// the ping-pong kernel at the end of this file (two product groups per SM,
+// cp.async staging a product ahead, TMEM twiddles).
+//
+// Design of the first two: half the bytes of a complex128 working set, so the accumulator and
 // one vector spectrum both stay in registers (no TMEM needed) and the FP32
 // pipe (2x the FP64 rate on B200) does the butterflies.  Latency is hidden by
 // occupancy: several independent products per SM, each a CTA group of T
