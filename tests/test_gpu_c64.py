@@ -76,3 +76,28 @@ def test_c64_mixed_precision_and_two_level_rejected():
     xb = torch.zeros((1, 3000), dtype=torch.complex64, device="cuda")
     with pytest.raises(NotImplementedError):
         batched.hankel_tvp_partial(hb, [xb, xb], (3000,) * 3)
+
+
+@pytest.mark.parametrize("shape,B", [((1024,) * 4, 1), ((1024,) * 4, 151), ((1024,) * 4, 299),
+                                     ((1000, 1024, 1024, 1024), 5),   # even d_H: 16-byte rows
+                                     ((800,) * 5, 3), ((1024, 1024, 1024), 150),
+                                     ((1024, 700, 700), 8), ((333, 777, 777, 777), 4)])
+def test_c64_pingpong_kernel_shapes(shape, B, monkeypatch):
+    """The complex64 ping-pong kernel (one repeated vector, L = 4096, x and y
+    within the first quarter): batch sizes around the grid size (tails of one
+    and two groups), odd and even generator lengths, orders 3-5; and the same
+    launch on the fast kernel (HK_NO_PP_C64=1) as a cross-check."""
+    rng = np.random.default_rng(sum(shape) + B)
+    d = sum(shape) - len(shape) + 1
+    assert 2048 < d <= 4096 and max(shape[1:]) <= 1024 and shape[0] <= 1024
+    h = _c64(rng.standard_normal((B, d)) + 1j * rng.standard_normal((B, d)))
+    x = _c64(rng.standard_normal((B, shape[1])) + 1j * rng.standard_normal((B, shape[1])))
+    dh, dx = torch.from_numpy(h).cuda(), torch.from_numpy(x).cuda()
+    y = batched.hankel_tvp_partial(dh, [dx] * (len(shape) - 1), shape).cpu().numpy()
+    monkeypatch.setenv("HK_NO_PP_C64", "1")
+    y2 = batched.hankel_tvp_partial(dh, [dx] * (len(shape) - 1), shape).cpu().numpy()
+    assert strict_relerr(y, y2) <= 1e-5
+    c = lambda v: v.astype(np.complex128)
+    for b in sorted({0, B // 2, B - 1}):
+        ref = O.hankel_tvp_partial(c(h[b]), shape, [c(x[b])] * (len(shape) - 1))
+        assert strict_relerr(y[b], ref) <= TOL
