@@ -493,7 +493,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": statistics.median(ts) * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": WORKLOAD, "batch": BATCH, "n": N_MODE, "order": ORDER,
                    "fft_len": FFT_LEN},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
