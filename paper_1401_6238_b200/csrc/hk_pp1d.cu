@@ -139,8 +139,10 @@ template <bool ROWS>
 __device__ __forceinline__ long long pp_off(const Args1D &a, long long b, long long bs,
                                             long long ss) {
   if (!ROWS || a.nsub == 1) return b * bs;  // plain batches launch with nsub == 1
-  const long long ob = b / a.nsub;
-  return ob * bs + (b - ob * a.nsub) * ss;
+  // launch items and nsub fit 32 bits (checked at launch): one 32-bit division
+  // instead of the emulated 64-bit one
+  const unsigned ob = (unsigned)b / (unsigned)a.nsub;
+  return ob * bs + ((unsigned)b - ob * (unsigned)a.nsub) * ss;
 }
 
 // XD (NZ == R0: x is a full-length row, the two-level row stage): x is not
@@ -481,6 +483,7 @@ static cudaError_t launch_pp(const Args1D &a, cudaStream_t stream) {
     cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
     configured.fetch_or(bit);
   }
+  if (a.batch >= (1ll << 31) || a.nsub >= (1ll << 31)) return cudaErrorNotSupported;
   long long grid = sms[dev & 63];
   if (const char *e = getenv("HK_PP_GRID")) grid = atoi(e);
   if (grid > a.batch) grid = a.batch;
@@ -572,9 +575,9 @@ __global__ void __launch_bounds__(512, 1) k_rows_pp(const __grid_constant__ Args
 
   const long long nunits = (a.batch + GP - 1) / GP;
   const long long nloc = nunits > blockIdx.x ? (nunits - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  auto row_off = [&](long long b, long long bs, long long ss) {
-    const long long ob = b / a.nsub;
-    return ob * bs + (b - ob * a.nsub) * ss;
+  auto row_off = [&](long long b, long long bs, long long ss) {  // 32-bit: see launch_rows_pp
+    const unsigned ob = (unsigned)b / (unsigned)a.nsub;
+    return ob * bs + ((unsigned)b - ob * (unsigned)a.nsub) * ss;
   };
   struct Unit {
     long long b0;
@@ -701,6 +704,7 @@ static cudaError_t launch_rows_pp(const Args1D &a, cudaStream_t stream) {
     cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
     configured.fetch_or(bit);
   }
+  if (a.batch >= (1ll << 31) || a.nsub >= (1ll << 31)) return cudaErrorNotSupported;
   const long long units = (a.batch + GP - 1) / GP;
   long long grid = std::min<long long>(units, sms[dev & 63]);
   if (grid <= 0) return cudaSuccess;
