@@ -43,7 +43,8 @@ constexpr bool kTw0Rec = true;
 __device__ __forceinline__ void prefetch_item(const Factor &f, long long b, long long nsub,
                                               int kind_bytes) {
   if (f.kind == FK_SPEC || f.estride != 1 || f.len <= 0) return;
-  const long long ob = b / nsub, os = b - ob * nsub;
+  long long ob, os;
+  split_item(b, nsub, ob, os);
   const char *p = static_cast<const char *>(f.ptr) + (ob * f.bstride + os * f.sstride) * kind_bytes;
   unsigned bytes = (unsigned)f.len * (unsigned)kind_bytes;
   // 16-byte aligned start and size
@@ -154,7 +155,8 @@ __global__ void __launch_bounds__(PL::CTA, (min_blocks_for<PL, STG>()))
   auto stage_issue = [&](const Factor &f, long long bb, int k0, int nin, int fac_idx) {
     long long b = bb * PL::G + g;
     if (b >= a.batch) b = a.batch - 1;
-    const long long ob = b / a.nsub, os = b - ob * a.nsub;
+    long long ob, os;
+    split_item(b, a.nsub, ob, os);
     const long long col = (fac_idx >= 0 && a.ncombo) ? (long long)a.combo_col[os][fac_idx] : os;
     const long long off = ob * f.bstride + col * f.sstride;
     const bool f64 = f.kind == FK_F64;
@@ -200,7 +202,8 @@ __global__ void __launch_bounds__(PL::CTA, (min_blocks_for<PL, STG>()))
     long long b = bb * PL::G + g;
     const bool active = b < a.batch;
     if (!active) b = a.batch - 1;
-    const long long ob = b / a.nsub, os = b - ob * a.nsub;
+    long long ob, os;
+    split_item(b, a.nsub, ob, os);
 
     cplx v[V];
     cplx *out = static_cast<cplx *>(a.out) + ob * a.out_bstride +

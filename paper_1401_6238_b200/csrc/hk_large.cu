@@ -142,8 +142,9 @@ __global__ void __launch_bounds__(TILE * PL::T, (col_blocks<PL, TILE>())) k_cols
   const uint32_t is1 = (uint32_t)a.in.s1, is2 = (uint32_t)a.in.s2;
   const uint32_t is1b = PAIR ? (uint32_t)a.in2.s1 : 0u, is2b = PAIR ? (uint32_t)a.in2.s2 : 0u;
   auto issue = [&](long long w, cplx *tile) {
-    const long long item = w / tiles_per_item;
-    const int c0 = (int)(w - item * tiles_per_item) * TILE;
+    // tile indices fit 32 bits (launch_cols_t): no emulated 64-bit division
+    const long long item = (unsigned)w / (unsigned)tiles_per_item;
+    const int c0 = (int)((unsigned)w - (unsigned)item * (unsigned)tiles_per_item) * TILE;
     const bool half_c = STAGE == ST_C && a.half;
     const int esz = real_in || PAIR ? 8 : 16;
     const char *b1 = static_cast<const char *>(a.in.ptr) + item * a.in.item_stride * esz;
@@ -217,8 +218,8 @@ __global__ void __launch_bounds__(TILE * PL::T, (col_blocks<PL, TILE>())) k_cols
       cp_async_wait<0>();
     }
     __syncthreads();
-    const long long item = w / tiles_per_item;
-    const int c0 = (int)(w - item * tiles_per_item) * TILE;
+    const long long item = (unsigned)w / (unsigned)tiles_per_item;
+    const int c0 = (int)((unsigned)w - (unsigned)item * (unsigned)tiles_per_item) * TILE;
     const int n2 = c0 + c;
     cplx *col = tile + c * CS;
     // pass-0 input: scale, real promotion, stage-C twiddle.  The elements of a
@@ -422,6 +423,7 @@ static cudaError_t launch_cols_t(const ColArgs &a, long long items, int ncols,
   const int tiles = (ncols + TILE - 1) / TILE;
   const long long ntiles = (long long)tiles * items;
   if (ntiles <= 0) return cudaSuccess;
+  if (ntiles >= (1ll << 31)) return cudaErrorNotSupported;
   const long long grid = std::min<long long>(ntiles, resident[dev & 63]);
   k_cols<PL, TILE, STAGE><<<(unsigned)grid, TILE * PL::T, smem, stream>>>(a, tiles, ntiles);
   return cudaGetLastError();
