@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(PL::CTA, 1) k_hankel_1d(const __grid_constant_
   long long b = (long long)blockIdx.x * PL::G + g;
   const bool active = b < a.batch;
   if (!active) b = a.batch - 1;  // idle groups shadow a valid item; their stores are masked
-  const long long ob = b / a.nsub, os = b - (b / a.nsub) * a.nsub;
+  long long ob, os;
+  split_item(b, a.nsub, ob, os);
   cplx *sbuf = smem + (PL::P > 1 ? g * PL::L : 0);
   const cplx *__restrict__ tw = a.tw;
   uint32_t tmy = 0;

@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(PL::CTA, (C64Tr<PL>::min_blocks))
     long long b = bb * PL::G + g;
     const bool active = b < a.batch;
     if (!active) b = a.batch - 1;  // idle groups shadow a valid item; stores are masked
-    const long long ob = b / a.nsub, os = b - ob * a.nsub;
+    long long ob, os;
+    split_item(b, a.nsub, ob, os);
 
     cplxf acc[Tr::tmem ? 1 : V];
     cplxf v[V];
@@ -199,7 +200,8 @@ static int resident_ctas(const void *fn, int cta, int smem, int dev) {
 __device__ __forceinline__ void prefetch_f(const Factor &f, long long b, long long nsub) {
   if (f.estride != 1 || f.len <= 0) return;
   const int eb = f.kind == FK_F32 ? 4 : 8;
-  const long long ob = b / nsub, os = b - ob * nsub;
+  long long ob, os;
+  split_item(b, nsub, ob, os);
   const char *p = static_cast<const char *>(f.ptr) + (ob * f.bstride + os * f.sstride) * eb;
   const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
   const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p) + (unsigned)f.len * eb + 15) &
@@ -258,7 +260,8 @@ __global__ void __launch_bounds__(PL::CTA, (FastC64Tr<PL>::min_blocks))
     long long b = bb * PL::G + g;
     const bool active = b < a.batch;
     if (!active) b = a.batch - 1;
-    const long long ob = b / a.nsub, os = b - ob * a.nsub;
+    long long ob, os;
+    split_item(b, a.nsub, ob, os);
     cplxf v[V];
     {
       const Factor &hf = a.h;
